@@ -1,0 +1,156 @@
+/* include/aegis.h -- C-ABI of libaegis, the B200-native executor of the AEGIS
+ * CKKS hot path (arXiv 2604.03425).  Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary; no exceptions escape it.
+ *
+ * The reference (/root/reference/proj/include/heplan/, header-only C++20) has
+ * no executor: SPEC.md:392-443 specifies one (`rns-oracle`: exec_sequential /
+ * exec_plan) over the IR of poly_ir.hpp / he_ir.hpp.  Each entry point below
+ * replaces the reference interface cited beside it (INTEGRATION.md shows the
+ * binding a heplan maintainer would add).
+ *
+ * Data layout: a bundle is a [lane][comp][limb][N] array of
+ * u64 residues; limb i of every bundle is modulo the main prime q_i, values
+ * canonical in [0, p), polynomials in the NTT (evaluation) domain.
+ *
+ * Errors: every call returns 0 on success or one of the AEGIS_E* codes; the
+ * message is available from aegis_last_error(ctx).  The C++ wrapper
+ * (paper_2604_03425_b200/csrc/heplan_compat.hpp) rethrows them as the
+ * reference's exception types: EINVAL -> std::invalid_argument,
+ * ELOGIC -> std::logic_error, others -> std::runtime_error.
+ * Threading: one host thread per context; all work is asynchronous on the
+ * context's compute stream; errors from the device surface at aegis_sync().
+ */
+#ifndef AEGIS_H
+#define AEGIS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AEGIS_OK 0
+#define AEGIS_EINVAL 1 /* std::invalid_argument in the reference (ckks.hpp:149, graph.hpp:100) */
+#define AEGIS_ELOGIC 2 /* std::logic_error (he_ir.hpp:191) */
+#define AEGIS_ECUDA 3
+#define AEGIS_ENCCL 4
+#define AEGIS_EOOM 5
+
+typedef struct aegis_ctx aegis_ctx;
+typedef struct aegis_bundle aegis_bundle;
+typedef struct aegis_graph aegis_graph;
+
+/* CkksProfile (ckks.hpp:21-46) plus the seeds of the synthetic workload. */
+typedef struct aegis_params {
+  uint32_t log_n;           /* ring_degree = 2^log_n, 4..17 */
+  uint32_t chain_length;    /* |Q_L| main primes (35 for BERT) */
+  uint32_t special_primes;  /* |P|; must be 4 (AEGIS_SPECIAL_PRIMES) */
+  uint32_t bootstrap_level; /* l_boot (14) -> post_boot_level = chain - l_boot */
+  uint64_t seed_input;      /* graph-input ciphertexts (PRNG tag 1) */
+  uint64_t seed_weight;     /* kGenerate weights (tag 2) */
+  uint64_t seed_key;        /* key-switching keys (tag 3) */
+} aegis_params;
+
+/* ---- context (one per GPU) ----------------------------------------------- */
+int aegis_ctx_create(const aegis_params* params, int device, aegis_ctx** out);
+int aegis_ctx_destroy(aegis_ctx* ctx);
+const char* aegis_last_error(const aegis_ctx* ctx);
+void* aegis_stream_compute(aegis_ctx* ctx); /* cudaStream_t */
+void* aegis_stream_comm(aegis_ctx* ctx);    /* cudaStream_t for collectives */
+int aegis_sync(aegis_ctx* ctx);
+uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t ext_index); /* <60 main, >=60 special */
+/* count of kernels this context launched (for the bench's gpu_launches claim) */
+uint64_t aegis_launch_count(const aegis_ctx* ctx);
+
+/* ---- bundles (CtBundle, he_ir.hpp:57-74) --------------------------------- */
+int aegis_bundle_alloc(aegis_ctx* ctx, uint32_t lanes, uint32_t comps, uint32_t level,
+                       aegis_bundle** out);
+int aegis_bundle_free(aegis_ctx* ctx, aegis_bundle* b);
+/* count must equal lanes*comps*level*N; host buffers are caller owned */
+int aegis_bundle_upload(aegis_ctx* ctx, aegis_bundle* b, const uint64_t* host, uint64_t count);
+int aegis_bundle_download(aegis_ctx* ctx, const aegis_bundle* b, uint64_t* host, uint64_t count);
+int aegis_bundle_info(const aegis_bundle* b, uint32_t* lanes, uint32_t* comps, uint32_t* level,
+                      uint64_t* device_ptr);
+/* synthetic "fresh activations" (he_ir.hpp:178-188): PRNG tag 1 keyed by bundle_id */
+int aegis_bundle_fill_input(aegis_ctx* ctx, aegis_bundle* b, uint32_t bundle_id);
+/* DESIGN.md §2.4 content hash of the first `comps` comps and `level` limbs */
+int aegis_bundle_hash(aegis_ctx* ctx, const aegis_bundle* b, uint32_t comps, uint32_t level,
+                      uint64_t* out);
+
+/* ---- keys (poly_ir.hpp:300-305: 0 = relin, 1000 + r = rotation r) -------- */
+int aegis_keys_generate(aegis_ctx* ctx, const uint64_t* key_ids, uint32_t count);
+int aegis_keys_bytes(const aegis_ctx* ctx, uint64_t* out);
+
+/* ---- polynomial instructions (PolyOpKind, poly_ir.hpp:23-32) -------------
+ * FragSpan-style addressing (poly_ir.hpp:87-99): lanes [lane, lane+lane_count)
+ * and limbs [prime_lo, prime_hi] of every component of bundle b.          */
+int aegis_ntt(aegis_ctx* ctx, aegis_bundle* b, uint32_t lane, uint32_t lane_count,
+              uint32_t prime_lo, uint32_t prime_hi, int inverse); /* kNtt / kIntt */
+/* kAutomorphism: eval-domain x -> x^galois of the first `level` limbs */
+int aegis_automorphism(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* in, uint32_t lane,
+                       uint32_t lane_count, uint32_t level, uint64_t galois);
+/* exact centred basis conversion on coefficient-domain limbs (kModUp/kModDown
+ * semantics): out limb dst_limb[t] of every lane/comp gets
+ * lift_centered(in[src_limb[0..k)]) mod prime(dst_ext[t]).  src/dst ext indices
+ * name the primes; src_limb/dst_limb the limb positions inside the bundles.  */
+int aegis_basis_convert(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* in,
+                        const uint32_t* src_ext, const uint32_t* src_limb, uint32_t k,
+                        const uint32_t* dst_ext, const uint32_t* dst_limb, uint32_t m);
+/* hybrid key switch of component `comp` of every lane (poly_ir.hpp:219-298):
+ * out (2 comps, level limbs) = KS(in[comp]) with key key_id */
+int aegis_keyswitch(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* in, uint32_t comp,
+                    uint32_t level, uint64_t key_id);
+
+/* ---- HE operators (HeOpKind, he_ir.hpp:21-31), one call per bundled HeOp --
+ * Operand lanes follow emit_per_lane (he_ir.hpp:200-222): output lane l reads
+ * operand lane  lane0 + (count == lanes ? l : l % count).                  */
+int aegis_rot(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
+              uint32_t in_lane, uint32_t lanes, uint32_t level, int offset);
+int aegis_relin(aegis_ctx* ctx, aegis_bundle* b, uint32_t lane, uint32_t lanes, uint32_t level);
+int aegis_rescale(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
+                  uint32_t in_lane, uint32_t lanes, uint32_t level);
+int aegis_boot(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
+               uint32_t in_lane, uint32_t lanes, uint32_t level, uint32_t out_level);
+int aegis_cmult(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, uint32_t lanes,
+                const aegis_bundle* a, uint32_t a_lane, uint32_t a_count, const aegis_bundle* b,
+                uint32_t b_lane, uint32_t b_count, uint32_t level);
+/* accumulate != 0: out[l] += a[..]; else out[l] = a[..] + b[..] */
+int aegis_cadd(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, uint32_t lanes,
+               const aegis_bundle* a, uint32_t a_lane, uint32_t a_count, const aegis_bundle* b,
+               uint32_t b_lane, uint32_t b_count, uint32_t level, int accumulate);
+/* bundled PMult-accumulate (he_ir.hpp:360-371) with in-kernel kGenerate
+ * weights of bundle weight_bundle_id; chunk_period as in
+ * CtBundle::chunk_period of the accumulator (0 = whole). */
+int aegis_pmult_acc(aegis_ctx* ctx, aegis_bundle* acc, uint32_t acc_lane, uint32_t acc_lanes,
+                    uint32_t chunk_period, const aegis_bundle* x, uint32_t x_lane, uint32_t x_lanes,
+                    uint32_t weight_bundle_id, uint32_t weight_lanes, uint32_t level);
+
+/* ---- layer drivers + executor (he_ir.hpp:683 lower_app_to_he; SPEC exec_*) */
+typedef struct aegis_model {
+  uint32_t kind;        /* 0: transformer blocks (graph.hpp:168), 1: FFN only (config 1) */
+  uint32_t layers;      /* TransformerConfig::layer_count */
+  uint32_t model_dim, ffn_dim, head_dim, slots_per_token;
+  uint64_t tokens;
+} aegis_model;
+int aegis_graph_build(aegis_ctx* ctx, const aegis_model* model, aegis_graph** out);
+/* same, without a device (planning only): the lowering is host code */
+int aegis_graph_build_params(const aegis_params* params, const aegis_model* model, aegis_graph** out);
+int aegis_graph_load(aegis_ctx* ctx, const char* path, aegis_graph** out); /* heops text */
+int aegis_graph_dump(const aegis_graph* g, const char* path);
+int aegis_graph_info(const aegis_graph* g, uint64_t* ops, uint64_t* bundles);
+/* Restrict execution to token groups [tg_lo, tg_hi) of `tg_total` (lane
+ * ownership for multi-GPU token-coherent placement, placement.hpp:175-182). */
+int aegis_graph_set_shard(aegis_graph* g, uint32_t tg_lo, uint32_t tg_hi);
+/* Execute ops [0, max_ops) (all if < 0).  Bundles are allocated at first write
+ * and freed after their last use.  If hashes != NULL, hashes[b] receives the
+ * content hash of bundle b when it dies (0 if never materialised). */
+int aegis_graph_run(aegis_ctx* ctx, aegis_graph* g, int64_t max_ops, uint64_t* hashes,
+                    uint64_t nhashes);
+/* key ids the graph needs (for aegis_keys_generate); returns count via *n */
+int aegis_graph_key_ids(const aegis_graph* g, uint64_t* ids, uint32_t cap, uint32_t* n);
+int aegis_graph_free(aegis_graph* g);
+/* peak device bytes of the last aegis_graph_run */
+uint64_t aegis_graph_peak_bytes(const aegis_graph* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,93 @@
+"""ctypes binding of libaegis (include/aegis.h).
+
+The shared library is built in-tree (paper_2604_03425_b200/libaegis.so) by
+__graft_entry__.build().  There is deliberately no fallback: if the library is
+missing, importing the product API raises immediately.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaegis.so")
+
+u32 = ctypes.c_uint32
+u64 = ctypes.c_uint64
+i64 = ctypes.c_int64
+vp = ctypes.c_void_p
+u64p = ctypes.POINTER(ctypes.c_uint64)
+u32p = ctypes.POINTER(ctypes.c_uint32)
+
+AEGIS_OK, AEGIS_EINVAL, AEGIS_ELOGIC, AEGIS_ECUDA, AEGIS_ENCCL, AEGIS_EOOM = range(6)
+
+
+class AegisParams(ctypes.Structure):
+    _fields_ = [("log_n", u32), ("chain_length", u32), ("special_primes", u32),
+                ("bootstrap_level", u32), ("seed_input", u64), ("seed_weight", u64),
+                ("seed_key", u64)]
+
+
+class AegisModel(ctypes.Structure):
+    _fields_ = [("kind", u32), ("layers", u32), ("model_dim", u32), ("ffn_dim", u32),
+                ("head_dim", u32), ("slots_per_token", u32), ("tokens", u64)]
+
+
+# (name, restype, argtypes) for every function declared in include/aegis.h
+SIGNATURES = [
+    ("aegis_ctx_create", ctypes.c_int, [ctypes.POINTER(AegisParams), ctypes.c_int, ctypes.POINTER(vp)]),
+    ("aegis_ctx_destroy", ctypes.c_int, [vp]),
+    ("aegis_last_error", ctypes.c_char_p, [vp]),
+    ("aegis_stream_compute", vp, [vp]),
+    ("aegis_stream_comm", vp, [vp]),
+    ("aegis_sync", ctypes.c_int, [vp]),
+    ("aegis_prime", u64, [vp, u32]),
+    ("aegis_launch_count", u64, [vp]),
+    ("aegis_bundle_alloc", ctypes.c_int, [vp, u32, u32, u32, ctypes.POINTER(vp)]),
+    ("aegis_bundle_free", ctypes.c_int, [vp, vp]),
+    ("aegis_bundle_upload", ctypes.c_int, [vp, vp, u64p, u64]),
+    ("aegis_bundle_download", ctypes.c_int, [vp, vp, u64p, u64]),
+    ("aegis_bundle_info", ctypes.c_int, [vp, u32p, u32p, u32p, u64p]),
+    ("aegis_bundle_fill_input", ctypes.c_int, [vp, vp, u32]),
+    ("aegis_bundle_hash", ctypes.c_int, [vp, vp, u32, u32, u64p]),
+    ("aegis_keys_generate", ctypes.c_int, [vp, u64p, u32]),
+    ("aegis_keys_bytes", ctypes.c_int, [vp, u64p]),
+    ("aegis_ntt", ctypes.c_int, [vp, vp, u32, u32, u32, u32, ctypes.c_int]),
+    ("aegis_automorphism", ctypes.c_int, [vp, vp, vp, u32, u32, u32, u64]),
+    ("aegis_basis_convert", ctypes.c_int, [vp, vp, vp, u32p, u32p, u32, u32p, u32p, u32]),
+    ("aegis_keyswitch", ctypes.c_int, [vp, vp, vp, u32, u32, u64]),
+    ("aegis_rot", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32, ctypes.c_int]),
+    ("aegis_relin", ctypes.c_int, [vp, vp, u32, u32, u32]),
+    ("aegis_rescale", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32]),
+    ("aegis_boot", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32, u32]),
+    ("aegis_cmult", ctypes.c_int, [vp, vp, u32, u32, vp, u32, u32, vp, u32, u32, u32]),
+    ("aegis_cadd", ctypes.c_int, [vp, vp, u32, u32, vp, u32, u32, vp, u32, u32, u32, ctypes.c_int]),
+    ("aegis_pmult_acc", ctypes.c_int, [vp, vp, u32, u32, u32, vp, u32, u32, u32, u32, u32]),
+    ("aegis_graph_build", ctypes.c_int, [vp, ctypes.POINTER(AegisModel), ctypes.POINTER(vp)]),
+    ("aegis_graph_build_params", ctypes.c_int,
+     [ctypes.POINTER(AegisParams), ctypes.POINTER(AegisModel), ctypes.POINTER(vp)]),
+    ("aegis_graph_load", ctypes.c_int, [vp, ctypes.c_char_p, ctypes.POINTER(vp)]),
+    ("aegis_graph_dump", ctypes.c_int, [vp, ctypes.c_char_p]),
+    ("aegis_graph_info", ctypes.c_int, [vp, u64p, u64p]),
+    ("aegis_graph_set_shard", ctypes.c_int, [vp, u32, u32]),
+    ("aegis_graph_run", ctypes.c_int, [vp, vp, i64, u64p, u64]),
+    ("aegis_graph_key_ids", ctypes.c_int, [vp, u64p, u32, u32p]),
+    ("aegis_graph_free", ctypes.c_int, [vp]),
+    ("aegis_graph_peak_bytes", u64, [vp]),
+]
+
+_lib = None
+
+
+def load():
+    """Load libaegis.so (raises OSError if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OSError(f"{LIB_PATH} is missing: run __graft_entry__.build() first "
+                          "(there is no CPU fallback for the product path)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib

@@ -1,0 +1,284 @@
+"""Python host API of libaegis, mirroring the reference's operator surface.
+
+Reference mapping (proj/include/heplan/):
+  Context      -- one GPU + CkksProfile (ckks.hpp:21-46) + keys/tables
+  Bundle       -- CtBundle (he_ir.hpp:57-74): [lane][comp][limb][N] u64 on device
+  Context.rot / relin / rescale / boot / cmult / cadd / pmult_acc
+               -- HeOpKind evaluator ops (he_ir.hpp:21-31), bundled form
+  Context.ntt / automorphism / basis_convert / keyswitch
+               -- PolyOpKind instructions (poly_ir.hpp:23-32)
+  Graph        -- HeOpGraph from lower_app_to_he (he_ir.hpp:683) + executor
+                  (SPEC.md:407-415 exec_sequential)
+Errors raise the reference's exception types: EINVAL -> ValueError
+(std::invalid_argument), ELOGIC -> RuntimeError subclass LogicError
+(std::logic_error), CUDA/NCCL/OOM -> AegisError.
+"""
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+
+BERT_PARAMS = dict(log_n=16, chain_length=35, special_primes=4, bootstrap_level=14)
+SEED_INPUT = 0xAE615
+SEED_WEIGHT = 0xAE616
+SEED_KEY = 0xAE617
+
+
+class AegisError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"aegis error {code}: {msg}")
+        self.code = code
+
+
+class LogicError(AegisError):
+    pass
+
+
+def _raise(code, msg):
+    if code == L.AEGIS_EINVAL:
+        raise ValueError(msg)
+    if code == L.AEGIS_ELOGIC:
+        raise LogicError(code, msg)
+    raise AegisError(code, msg)
+
+
+def _u64p(a):
+    return a.ctypes.data_as(L.u64p)
+
+
+def _u32arr(xs):
+    a = np.ascontiguousarray(np.asarray(xs, dtype=np.uint32))
+    return a, a.ctypes.data_as(L.u32p)
+
+
+class Bundle:
+    def __init__(self, ctx, handle, lanes, comps, level):
+        self.ctx, self.h, self.lanes, self.comps, self.level = ctx, handle, lanes, comps, level
+
+    @property
+    def shape(self):
+        return (self.lanes, self.comps, self.level, self.ctx.n)
+
+    def upload(self, arr):
+        a = np.ascontiguousarray(arr, dtype=np.uint64)
+        if a.shape != self.shape:
+            raise ValueError(f"upload shape {a.shape} != {self.shape}")
+        self.ctx._call("aegis_bundle_upload", self.h, _u64p(a), a.size)
+
+    def download(self):
+        a = np.empty(self.shape, dtype=np.uint64)
+        self.ctx._call("aegis_bundle_download", self.h, _u64p(a), a.size)
+        return a
+
+    def hash(self, comps=None, level=None):
+        out = ctypes.c_uint64()
+        self.ctx._call("aegis_bundle_hash", self.h, self.comps if comps is None else comps,
+                       self.level if level is None else level, ctypes.byref(out))
+        return out.value
+
+    def fill_input(self, bundle_id):
+        self.ctx._call("aegis_bundle_fill_input", self.h, bundle_id)
+
+    def device_ptr(self):
+        p = ctypes.c_uint64()
+        L.load().aegis_bundle_info(self.h, None, None, None, ctypes.byref(p))
+        return p.value
+
+    def free(self):
+        if self.h:
+            self.ctx._call("aegis_bundle_free", self.h)
+            self.h = None
+
+
+class Context:
+    """One B200 running the CKKS hot path (a CkksProfile plus device state)."""
+
+    def __init__(self, log_n=16, chain_length=35, bootstrap_level=14, device=0,
+                 seed_input=SEED_INPUT, seed_weight=SEED_WEIGHT, seed_key=SEED_KEY):
+        self.lib = L.load()
+        self.params = L.AegisParams(log_n, chain_length, 4, bootstrap_level, seed_input,
+                                    seed_weight, seed_key)
+        h = ctypes.c_void_p()
+        rc = self.lib.aegis_ctx_create(ctypes.byref(self.params), device, ctypes.byref(h))
+        if rc != L.AEGIS_OK:
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+        self.h = h
+        self.n = 1 << log_n
+        self.log_n = log_n
+        self.chain = chain_length
+
+    def _call(self, name, *args):
+        rc = getattr(self.lib, name)(self.h, *args)
+        if rc != L.AEGIS_OK:
+            _raise(rc, self.lib.aegis_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.aegis_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- misc --
+    def prime(self, ext):
+        return self.lib.aegis_prime(self.h, ext)
+
+    def sync(self):
+        self._call("aegis_sync")
+
+    @property
+    def stream(self):
+        return self.lib.aegis_stream_compute(self.h)
+
+    def launch_count(self):
+        return self.lib.aegis_launch_count(self.h)
+
+    # -- bundles / keys --
+    def bundle(self, lanes, comps, level):
+        h = ctypes.c_void_p()
+        self._call("aegis_bundle_alloc", lanes, comps, level, ctypes.byref(h))
+        return Bundle(self, h, lanes, comps, level)
+
+    def keys_generate(self, ids):
+        a = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
+        self._call("aegis_keys_generate", _u64p(a), len(a))
+
+    # -- polynomial instructions --
+    def ntt(self, b, lane=0, lanes=None, lo=0, hi=None, inverse=False):
+        self._call("aegis_ntt", b.h, lane, b.lanes if lanes is None else lanes, lo,
+                   b.level - 1 if hi is None else hi, 1 if inverse else 0)
+
+    def automorphism(self, out, inp, galois, level=None, lane=0, lanes=None):
+        self._call("aegis_automorphism", out.h, inp.h, lane, inp.lanes if lanes is None else lanes,
+                   inp.level if level is None else level, galois)
+
+    def basis_convert(self, out, inp, src_ext, src_limb, dst_ext, dst_limb):
+        a, pa = _u32arr(src_ext)
+        b, pb = _u32arr(src_limb)
+        c, pc = _u32arr(dst_ext)
+        d, pd = _u32arr(dst_limb)
+        self._call("aegis_basis_convert", out.h, inp.h, pa, pb, len(a), pc, pd, len(c))
+
+    def keyswitch(self, out, inp, comp, level, key_id):
+        self._call("aegis_keyswitch", out.h, inp.h, comp, level, key_id)
+
+    # -- HE operators --
+    def rot(self, out, inp, offset, level, out_lane=0, in_lane=0, lanes=None):
+        self._call("aegis_rot", out.h, out_lane, inp.h, in_lane,
+                   inp.lanes if lanes is None else lanes, level, offset)
+
+    def relin(self, b, level, lane=0, lanes=None):
+        self._call("aegis_relin", b.h, lane, b.lanes if lanes is None else lanes, level)
+
+    def rescale(self, out, inp, level, out_lane=0, in_lane=0, lanes=None):
+        self._call("aegis_rescale", out.h, out_lane, inp.h, in_lane,
+                   inp.lanes if lanes is None else lanes, level)
+
+    def boot(self, out, inp, level, out_level, out_lane=0, in_lane=0, lanes=None):
+        self._call("aegis_boot", out.h, out_lane, inp.h, in_lane,
+                   inp.lanes if lanes is None else lanes, level, out_level)
+
+    def cmult(self, out, a, b, level, lanes=None, a_slice=None, b_slice=None, out_lane=0):
+        lanes = out.lanes if lanes is None else lanes
+        al, ac = a_slice or (0, a.lanes)
+        bl, bc = b_slice or (0, b.lanes)
+        self._call("aegis_cmult", out.h, out_lane, lanes, a.h, al, ac, b.h, bl, bc, level)
+
+    def cadd(self, out, a, b, level, accumulate=False, lanes=None, a_slice=None, b_slice=None,
+             out_lane=0):
+        lanes = out.lanes if lanes is None else lanes
+        al, ac = a_slice or (0, a.lanes)
+        if b is None:
+            bh, bl, bc = None, 0, 0
+        else:
+            bh = b.h
+            bl, bc = b_slice or (0, b.lanes)
+        self._call("aegis_cadd", out.h, out_lane, lanes, a.h, al, ac, bh, bl, bc, level,
+                   1 if accumulate else 0)
+
+    def pmult_acc(self, acc, x, weight_bundle, weight_lanes, level, chunk_period=0):
+        self._call("aegis_pmult_acc", acc.h, 0, acc.lanes, chunk_period, x.h, 0, x.lanes,
+                   weight_bundle, weight_lanes, level)
+
+    # -- graphs --
+    def graph(self, kind=0, tokens=128, layers=1, model_dim=768, ffn_dim=3072, head_dim=64,
+              slots_per_token=64):
+        m = L.AegisModel(kind, layers, model_dim, ffn_dim, head_dim, slots_per_token, tokens)
+        h = ctypes.c_void_p()
+        self._call("aegis_graph_build", ctypes.byref(m), ctypes.byref(h))
+        return Graph(self.lib, h, self)
+
+    def load_graph(self, path):
+        h = ctypes.c_void_p()
+        self._call("aegis_graph_load", str(path).encode(), ctypes.byref(h))
+        return Graph(self.lib, h, self)
+
+
+def plan_graph(log_n=16, chain_length=35, bootstrap_level=14, kind=0, tokens=128, layers=1,
+               model_dim=768, ffn_dim=3072, head_dim=64, slots_per_token=64):
+    """Lower a model to its HeOpGraph without a GPU (the layer drivers are host code)."""
+    lib = L.load()
+    p = L.AegisParams(log_n, chain_length, 4, bootstrap_level, 0, 0, 0)
+    m = L.AegisModel(kind, layers, model_dim, ffn_dim, head_dim, slots_per_token, tokens)
+    h = ctypes.c_void_p()
+    rc = lib.aegis_graph_build_params(ctypes.byref(p), ctypes.byref(m), ctypes.byref(h))
+    if rc != L.AEGIS_OK:
+        _raise(rc, lib.aegis_last_error(None).decode())
+    return Graph(lib, h, None)
+
+
+class Graph:
+    def __init__(self, lib, h, ctx):
+        self.lib, self.h, self.ctx = lib, h, ctx
+
+    def info(self):
+        o, b = ctypes.c_uint64(), ctypes.c_uint64()
+        self.lib.aegis_graph_info(self.h, ctypes.byref(o), ctypes.byref(b))
+        return o.value, b.value
+
+    def dump(self, path):
+        rc = self.lib.aegis_graph_dump(self.h, str(path).encode())
+        if rc:
+            raise ValueError(f"cannot dump graph to {path}")
+
+    def key_ids(self):
+        n = ctypes.c_uint32()
+        self.lib.aegis_graph_key_ids(self.h, None, 0, ctypes.byref(n))
+        a = np.zeros(n.value, dtype=np.uint64)
+        self.lib.aegis_graph_key_ids(self.h, _u64p(a), n.value, ctypes.byref(n))
+        return a
+
+    def set_shard(self, lo, hi):
+        rc = self.lib.aegis_graph_set_shard(self.h, lo, hi)
+        if rc:
+            raise ValueError("bad shard")
+
+    def run(self, max_ops=-1, hashes=False):
+        if self.ctx is None:
+            raise ValueError("graph was planned without a device context")
+        nb = self.info()[1]
+        if hashes:
+            h = np.zeros(nb, dtype=np.uint64)
+            self.ctx._call("aegis_graph_run", self.h, max_ops, _u64p(h), nb)
+            return h
+        self.ctx._call("aegis_graph_run", self.h, max_ops, None, 0)
+        return None
+
+    def peak_bytes(self):
+        return self.lib.aegis_graph_peak_bytes(self.h)
+
+    def free(self):
+        if self.h:
+            self.lib.aegis_graph_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -1,0 +1,118 @@
+// common.cuh -- shared device/host definitions for libaegis (sm_100a).
+//
+// Modular arithmetic for primes p < 2^48 (include/aegis_params.h) on 64-bit
+// words.  Semantics follow rns_math.hpp:21-40 (canonical results in [0, p));
+// the implementations are B200-specific:
+//   * Shoup multiplication by a precomputed constant (twiddles, CRT factors):
+//     one __umul64hi + two 64-bit mul.lo, result in [0, 2p) then one
+//     conditional subtract.
+//   * data x data products are accumulated as u128 and reduced once with a
+//     Barrett step valid for sums < 2^104 (up to 256 products of 48-bit
+//     residues) -- see reduce104().
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/aegis_params.h"
+
+namespace aegis {
+
+using u64 = unsigned long long;
+using u32 = unsigned int;
+
+constexpr u32 kSpecialBase = AEGIS_MAX_MAIN_PRIMES;  // ext index of P_0
+constexpr u32 kNumExt = AEGIS_MAX_MAIN_PRIMES + AEGIS_SPECIAL_PRIMES;
+constexpr u32 kAlpha = AEGIS_SPECIAL_PRIMES;  // digit width of hybrid key switching
+constexpr u64 kGold = 0x9E3779B97F4A7C15ULL;
+constexpr u64 kMixM = 0xD6E8FEB86659FD93ULL;
+
+// Per-prime constants (device resident, indexed by ext prime index).
+struct PrimeConst {
+  u64 p;
+  u64 mu104;   // floor(2^104 / p) for reduce104
+  u32 shift;   // 64 - bitlen(p): PRNG -> [0, 2p) mapping
+  u32 pad;
+};
+
+struct u128 {
+  u64 lo, hi;
+};
+
+__host__ __device__ __forceinline__ u64 mix64(u64 x) {
+  x ^= x >> 32;
+  x *= kMixM;
+  x ^= x >> 32;
+  x *= kMixM;
+  x ^= x >> 32;
+  return x;
+}
+
+// DESIGN.md §2.3 counter PRNG: row key per (seed, tag, a, b, c, d).
+__host__ __device__ __forceinline__ u64 row_key(u64 seed, u64 tag, u64 a, u64 b, u64 c, u64 d) {
+  u64 k = mix64(seed ^ (tag * kGold));
+  k = mix64(k ^ ((a + 1) * kGold));
+  k = mix64(k ^ ((b + 1) * kGold));
+  k = mix64(k ^ ((c + 1) * kGold));
+  k = mix64(k ^ ((d + 1) * kGold));
+  return k;
+}
+
+__host__ __device__ __forceinline__ u64 uniform_at(u64 rk, u64 i, u64 p, u32 shift) {
+  u64 v = mix64(rk + i * kGold) >> shift;
+  return v >= p ? v - p : v;
+}
+
+#ifdef __CUDACC__
+
+__device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 p) {
+  u64 s = a + b;
+  return s >= p ? s - p : s;
+}
+__device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 p) {
+  return a >= b ? a - b : a + p - b;
+}
+// a * w mod p with wp = floor(w 2^64 / p); valid for any a < 2^64.
+__device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wp, u64 p) {
+  const u64 q = __umul64hi(a, wp);
+  return a * w - q * p;  // in [0, 2p)
+}
+__device__ __forceinline__ u64 shoup(u64 a, u64 w, u64 wp, u64 p) {
+  const u64 r = shoup_lazy(a, w, wp, p);
+  return r >= p ? r - p : r;
+}
+
+__device__ __forceinline__ u128 mul_wide(u64 a, u64 b) {
+  u128 r;
+  r.lo = a * b;
+  r.hi = __umul64hi(a, b);
+  return r;
+}
+__device__ __forceinline__ void mac(u128& acc, u64 a, u64 b) {
+  const u64 lo = a * b;
+  const u64 hi = __umul64hi(a, b);
+  acc.lo += lo;
+  acc.hi += hi + (acc.lo < lo ? 1 : 0);
+}
+__device__ __forceinline__ void add_to(u128& acc, u64 a) {
+  acc.lo += a;
+  acc.hi += (acc.lo < a ? 1 : 0);
+}
+// s < 2^104  ->  s mod p  (p in (2^42, 2^48)).  q_est = floor((s >> 40) mu / 2^64)
+// is within 3 of floor(s / p) from below.
+__device__ __forceinline__ u64 reduce104(u128 s, u64 p, u64 mu) {
+  const u64 top = (s.lo >> 40) | (s.hi << 24);
+  const u64 q = __umul64hi(top, mu);
+  u64 r = s.lo - q * p;
+  r = r >= p ? r - p : r;
+  r = r >= p ? r - p : r;
+  r = r >= p ? r - p : r;
+  return r;
+}
+__device__ __forceinline__ u64 mul_mod(u64 a, u64 b, u64 p, u64 mu) {
+  return reduce104(mul_wide(a, b), p, mu);
+}
+
+#endif  // __CUDACC__
+
+}  // namespace aegis

@@ -1,0 +1,601 @@
+// context.cu -- device context, tables, keys, and the HE operators of libaegis.
+//
+// Host orchestration of the hot path.  Every operator is a short sequence of
+// sm_100a kernels on the context's compute stream; no CPU arithmetic touches
+// ciphertext data.  Reference anchors (proj/include/heplan/):
+//   NTT tables       rns_math.hpp:46-63, 103-117
+//   key switch       poly_ir.hpp:219-305 (Intt, Auto, ModUp, KeyMul, ModDown, Ntt)
+//   rescale          poly_ir.hpp:341-354 + div_round rns_math.hpp:196-202
+//   boot reset       poly_ir.hpp:355-368
+//   pointwise ops    poly_ir.hpp:192-213
+#include <algorithm>
+#include <cstring>
+
+#include "context.h"
+
+namespace aegis {
+
+namespace {
+
+using u128h = unsigned __int128;
+
+u64 h_mulmod(u64 a, u64 b, u64 p) { return (u64)(((u128h)a * b) % p); }
+u64 h_powmod(u64 b, u64 e, u64 p) {
+  u64 r = 1 % p;
+  b %= p;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, b, p);
+    b = h_mulmod(b, b, p);
+    e >>= 1;
+  }
+  return r;
+}
+u64 h_inv(u64 a, u64 p) { return h_powmod(a % p, p - 2, p); }
+u64 h_shoup(u64 w, u64 p) { return (u64)(((u128h)w << 64) / p); }
+u32 h_brev(u32 v, int bits) {
+  u32 r = 0;
+  for (int i = 0; i < bits; ++i, v >>= 1) r = (r << 1) | (v & 1);
+  return r;
+}
+
+// multiword helpers for conversion plans
+using Big = std::vector<u64>;
+void big_mul(Big& a, u64 m) {
+  u64 c = 0;
+  for (auto& w : a) {
+    u128h t = (u128h)w * m + c;
+    w = (u64)t;
+    c = (u64)(t >> 64);
+  }
+  if (c) a.push_back(c);
+}
+u64 big_mod(const Big& a, u64 p) {
+  u128h r = 0;
+  for (size_t i = a.size(); i-- > 0;) r = ((r << 64) | a[i]) % p;
+  return (u64)r;
+}
+
+}  // namespace
+
+Context::Context(const aegis_params& prm, int dev) {
+  if (prm.log_n < 4 || prm.log_n > AEGIS_MAX_LOG_N)
+    throw Error(AEGIS_EINVAL, "ring_degree must be a power of two in [2^4, 2^17]");
+  if (prm.chain_length == 0 || prm.chain_length > AEGIS_MAX_MAIN_PRIMES)
+    throw Error(AEGIS_EINVAL, "chain_length must be in [1, 60]");
+  if (prm.special_primes != AEGIS_SPECIAL_PRIMES)
+    throw Error(AEGIS_EINVAL, "special_prime_count must be 4");
+  if (prm.bootstrap_level > prm.chain_length)
+    throw Error(AEGIS_EINVAL, "bootstrap_level exceeds chain_length");  // ckks.hpp:45
+  log_n = prm.log_n;
+  n = 1u << log_n;
+  chain = prm.chain_length;
+  lboot = prm.bootstrap_level;
+  seed_input = prm.seed_input;
+  seed_weight = prm.seed_weight;
+  seed_key = prm.seed_key;
+  device = dev;
+  AEGIS_CHECK_CUDA(cudaSetDevice(dev));
+  AEGIS_CHECK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  AEGIS_CHECK_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+  AEGIS_CHECK_CUDA(cudaDeviceGetDefaultMemPool(&pool_, dev));
+  u64 thresh = ~0ull;  // keep freed blocks cached in the pool
+  AEGIS_CHECK_CUDA(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thresh));
+
+  for (u32 i = 0; i < AEGIS_MAX_MAIN_PRIMES; ++i) primes_.push_back(AEGIS_MAIN_PRIMES[i]);
+  for (u32 i = 0; i < AEGIS_SPECIAL_PRIMES; ++i) primes_.push_back(AEGIS_SPECIAL_PRIMES_LIST[i]);
+
+  // ---- per-prime constants + twiddle tables (rns_math.hpp:46-63) ----
+  std::vector<PrimeConst> pc(kNumExt);
+  std::vector<PrimeTw> tw(kNumExt);
+  std::vector<NttScale> sc(kNumExt);
+  const size_t tab_words = (size_t)n * 2;  // ulonglong2 per entry
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_twiddles_, (size_t)kNumExt * 2 * tab_words * sizeof(u64)));
+  std::vector<u64> hf(tab_words), hi(tab_words), pw(n), pwi(n);
+  for (u32 e = 0; e < kNumExt; ++e) {
+    const u64 p = primes_[e];
+    pc[e].p = p;
+    pc[e].mu104 = (u64)(((u128h)1 << 104) / p);
+    pc[e].shift = (u32)__builtin_clzll(p);
+    pc[e].pad = 0;
+    // psi: first g >= 2 whose g^((p-1)/2n) has order 2n (rns_math.hpp:103-111)
+    const u64 order = 2ull * n;
+    u64 psi = 0;
+    for (u64 g = 2; g < p; ++g) {
+      const u64 cand = h_powmod(g, (p - 1) / order, p);
+      if (h_powmod(cand, n, p) == p - 1) { psi = cand; break; }
+    }
+    if (!psi) throw Error(AEGIS_EINVAL, "no 2n-th root of unity found");
+    const u64 psi_inv = h_inv(psi, p);
+    pw[0] = pwi[0] = 1;
+    for (u32 i = 1; i < n; ++i) {
+      pw[i] = h_mulmod(pw[i - 1], psi, p);
+      pwi[i] = h_mulmod(pwi[i - 1], psi_inv, p);
+    }
+    for (u32 i = 0; i < n; ++i) {
+      const u32 r = h_brev(i, (int)log_n);
+      hf[2 * i] = pw[r];
+      hf[2 * i + 1] = h_shoup(pw[r], p);
+      hi[2 * i] = pwi[r];
+      hi[2 * i + 1] = h_shoup(pwi[r], p);
+    }
+    u64* fdev = d_twiddles_ + (size_t)e * 2 * tab_words;
+    u64* idev = fdev + tab_words;
+    AEGIS_CHECK_CUDA(cudaMemcpy(fdev, hf.data(), tab_words * 8, cudaMemcpyHostToDevice));
+    AEGIS_CHECK_CUDA(cudaMemcpy(idev, hi.data(), tab_words * 8, cudaMemcpyHostToDevice));
+    tw[e].fwd = reinterpret_cast<const ulonglong2*>(fdev);
+    tw[e].inv = reinterpret_cast<const ulonglong2*>(idev);
+    tw[e].p = p;
+    const u64 ninv = h_inv(n, p);
+    sc[e].n_inv = ninv;
+    sc[e].n_inv_p = h_shoup(ninv, p);
+    sc[e].w1n = h_mulmod(pwi[h_brev(1, (int)log_n)], ninv, p);  // inv[1] * N^{-1}
+    sc[e].w1n_p = h_shoup(sc[e].w1n, p);
+  }
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_pc, sizeof(PrimeConst) * kNumExt));
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_tw, sizeof(PrimeTw) * kNumExt));
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_scale, sizeof(NttScale) * kNumExt));
+  AEGIS_CHECK_CUDA(cudaMemcpy(d_pc, pc.data(), sizeof(PrimeConst) * kNumExt, cudaMemcpyHostToDevice));
+  AEGIS_CHECK_CUDA(cudaMemcpy(d_tw, tw.data(), sizeof(PrimeTw) * kNumExt, cudaMemcpyHostToDevice));
+  AEGIS_CHECK_CUDA(cudaMemcpy(d_scale, sc.data(), sizeof(NttScale) * kNumExt, cudaMemcpyHostToDevice));
+  std::vector<u32> ident(kNumExt);
+  for (u32 i = 0; i < kNumExt; ++i) ident[i] = i;
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_ident, sizeof(u32) * kNumExt));
+  AEGIS_CHECK_CUDA(cudaMemcpy(d_ident, ident.data(), sizeof(u32) * kNumExt, cudaMemcpyHostToDevice));
+  std::vector<u32> kse(key_slots());
+  for (u32 s = 0; s < key_slots(); ++s) kse[s] = s < chain ? s : kSpecialBase + (s - chain);
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_key_slot_ext_, sizeof(u32) * kse.size()));
+  AEGIS_CHECK_CUDA(cudaMemcpy(d_key_slot_ext_, kse.data(), sizeof(u32) * kse.size(), cudaMemcpyHostToDevice));
+}
+
+Context::~Context() {
+  cudaSetDevice(device);
+  cudaStreamSynchronize(stream);
+  for (auto& kv : keys_) cudaFree(kv.second);
+  for (auto& kv : plans_) cudaFree(kv.second.dev);
+  cudaFree(d_twiddles_);
+  cudaFree(d_pc);
+  cudaFree(d_tw);
+  cudaFree(d_scale);
+  cudaFree(d_ident);
+  cudaFree(d_key_slot_ext_);
+  cudaStreamDestroy(stream);
+  cudaStreamDestroy(comm);
+}
+
+u64* Context::alloc(size_t words) {
+  void* p = nullptr;
+  if (!words) words = 1;
+  cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(e == cudaErrorMemoryAllocation ? AEGIS_EOOM : AEGIS_ECUDA,
+                std::string("device allocation of ") + std::to_string(words * 8) + " bytes failed: " +
+                    cudaGetErrorString(e));
+  }
+  return static_cast<u64*>(p);
+}
+void Context::release(void* p) {
+  if (p) cudaFreeAsync(p, stream);
+}
+
+Bundle* Context::new_bundle(u32 lanes, u32 comps, u32 level, bool zero) {
+  auto* b = new Bundle;
+  b->lanes = lanes;
+  b->comps = comps;
+  b->level = level;
+  const size_t words = (size_t)lanes * comps * level * n;
+  b->bytes = words * 8;
+  try {
+    b->ptr = alloc(words);
+  } catch (...) {
+    delete b;
+    throw;
+  }
+  if (zero) AEGIS_CHECK_CUDA(cudaMemsetAsync(b->ptr, 0, b->bytes, stream));
+  live_bytes += b->bytes;
+  peak_bytes = std::max(peak_bytes, live_bytes);
+  return b;
+}
+void Context::free_bundle(Bundle* b) {
+  if (!b) return;
+  release(b->ptr);
+  live_bytes -= b->bytes;
+  delete b;
+}
+
+const Plan& Context::plan(const std::vector<u32>& src, const std::vector<u32>& dst) {
+  std::vector<u32> key(src);
+  key.push_back(0xffffffffu);
+  key.insert(key.end(), dst.begin(), dst.end());
+  auto it = plans_.find(key);
+  if (it != plans_.end()) return it->second;
+  const u32 k = (u32)src.size(), m = (u32)dst.size();
+  if (k == 0 || k > (u32)kMaxConv || m > (u32)kMaxConv) throw Error(AEGIS_EINVAL, "conversion basis too large");
+  ConvPlanDev h;
+  std::memset(&h, 0, sizeof(h));
+  h.k = k;
+  h.m = m;
+  Big B{1};
+  for (u32 i = 0; i < k; ++i) big_mul(B, prime(src[i]));
+  if (B.size() > (size_t)kMaxBigWords) throw Error(AEGIS_EINVAL, "conversion modulus too wide");
+  h.big_words = (u32)B.size();
+  for (size_t w = 0; w < B.size(); ++w) h.b_big[w] = B[w];
+  std::vector<u64> hm((size_t)k * m), hmp((size_t)k * m), hb((size_t)k * h.big_words, 0);
+  for (u32 i = 0; i < k; ++i) {
+    const u64 b = prime(src[i]);
+    Big hat{1};
+    for (u32 j = 0; j < k; ++j)
+      if (j != i) big_mul(hat, prime(src[j]));
+    for (size_t w = 0; w < hat.size() && w < h.big_words; ++w) hb[(size_t)i * h.big_words + w] = hat[w];
+    h.src_p[i] = b;
+    h.src_mu[i] = (u64)(((u128h)1 << 104) / b);
+    const u64 hinv = h_inv(big_mod(hat, b), b);
+    h.hat_inv[i] = hinv;
+    h.hat_inv_p[i] = h_shoup(hinv, b);
+    const u128h wq = (~(u128h)0) / b;  // floor(2^128 / b): b does not divide 2^128
+    h.w_hi[i] = (u64)(wq >> 64);
+    h.w_lo[i] = (u64)wq;
+    for (u32 t = 0; t < m; ++t) {
+      const u64 d = prime(dst[t]);
+      const u64 v = big_mod(hat, d);
+      hm[(size_t)i * m + t] = v;
+      hmp[(size_t)i * m + t] = h_shoup(v, d);
+    }
+  }
+  for (u32 t = 0; t < m; ++t) {
+    const u64 d = prime(dst[t]);
+    h.dst_p[t] = d;
+    h.dst_mu[t] = (u64)(((u128h)1 << 104) / d);
+    h.b_mod[t] = big_mod(B, d);
+  }
+  Plan pl;
+  pl.k = k;
+  pl.m = m;
+  const size_t extra = hm.size() + hmp.size() + hb.size();
+  char* mem = nullptr;
+  AEGIS_CHECK_CUDA(cudaMalloc(&mem, sizeof(ConvPlanDev) + extra * 8));
+  pl.dev = reinterpret_cast<ConvPlanDev*>(mem);
+  pl.tables = reinterpret_cast<u64*>(mem + sizeof(ConvPlanDev));
+  AEGIS_CHECK_CUDA(cudaMemcpy(pl.dev, &h, sizeof(h), cudaMemcpyHostToDevice));
+  AEGIS_CHECK_CUDA(cudaMemcpy(pl.tables, hm.data(), hm.size() * 8, cudaMemcpyHostToDevice));
+  AEGIS_CHECK_CUDA(cudaMemcpy(pl.tables + hm.size(), hmp.data(), hmp.size() * 8, cudaMemcpyHostToDevice));
+  if (!hb.empty())
+    AEGIS_CHECK_CUDA(cudaMemcpy(pl.tables + hm.size() + hmp.size(), hb.data(), hb.size() * 8,
+                                cudaMemcpyHostToDevice));
+  return plans_.emplace(key, pl).first->second;
+}
+
+void Context::generate_key(u64 key_id) {
+  if (keys_.count(key_id)) return;
+  u64* k = nullptr;
+  const size_t words = (size_t)key_digits() * 2 * key_slots() * n;
+  cudaError_t e = cudaMalloc(&k, words * 8);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(AEGIS_EOOM, "key allocation failed");
+  }
+  AEGIS_CHECK_CUDA(launch_fill_key(k, key_digits(), key_slots(), n, seed_key, key_id, d_key_slot_ext_, d_pc, stream));
+  count();
+  keys_[key_id] = k;
+}
+const u64* Context::key(u64 key_id) {
+  auto it = keys_.find(key_id);
+  if (it == keys_.end()) generate_key(key_id);
+  return keys_.at(key_id);
+}
+
+// ---------------------------------------------------------------------------
+void Context::ntt(u64* base, size_t lane_stride, u32 nlanes, const std::vector<u32>& slot_off,
+                  const std::vector<u32>& primes, bool inverse) {
+  if (slot_off.size() > (size_t)kMaxSlots) throw Error(AEGIS_EINVAL, "too many limbs in one NTT launch");
+  NttLaunch L;
+  std::memset(&L, 0, sizeof(L));
+  L.base = base;
+  L.lane_stride = lane_stride;
+  L.nlanes = nlanes;
+  L.nslots = (u32)slot_off.size();
+  L.n = n;
+  for (size_t i = 0; i < slot_off.size(); ++i) {
+    L.slot_off[i] = slot_off[i];
+    L.prime[i] = (unsigned char)primes[i];
+  }
+  L.tw = d_tw;
+  L.scale = d_scale;
+  // grid.x holds rows * ctas_per_row; split very large batches
+  const u32 max_rows = 1u << 20;
+  for (u32 l0 = 0; l0 < nlanes; ) {
+    u32 nl = std::max<u32>(1, std::min<u32>(nlanes - l0, max_rows / std::max<u32>(1, L.nslots)));
+    NttLaunch Lb = L;
+    Lb.base = base + (size_t)l0 * lane_stride;
+    Lb.nlanes = nl;
+    AEGIS_CHECK_CUDA(ntt_run(Lb, (int)log_n, inverse, stream));
+    count(2);
+    l0 += nl;
+  }
+}
+
+void Context::basis_convert(const u64* src, size_t src_ls, const std::vector<u32>& src_off,
+                            const std::vector<u32>& src_ext, u64* dst, size_t dst_ls,
+                            const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext, u32 lanes) {
+  const Plan& pl = plan(src_ext, dst_ext);
+  ConvIO io;
+  std::memset(&io, 0, sizeof(io));
+  io.src = src;
+  io.src_lane_stride = src_ls;
+  io.dst = dst;
+  io.dst_lane_stride = dst_ls;
+  for (size_t i = 0; i < src_off.size(); ++i) io.src_off[i] = src_off[i];
+  for (size_t i = 0; i < dst_off.size(); ++i) io.dst_off[i] = dst_off[i];
+  AEGIS_CHECK_CUDA(launch_basis_convert(pl.dev, pl.tables, io, lanes, n, pl.k, pl.m, stream));
+  count();
+}
+
+// ---------------------------------------------------------------------------
+// Hybrid key switching.  Lanes are processed in batches whose
+// workspace stays below ks_budget bytes; every kernel of a batch sees all of
+// its lanes, so each key limb is streamed once per batch.
+// ---------------------------------------------------------------------------
+void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id, const KsOut& o) {
+  if (l == 0 || l > chain) throw Error(AEGIS_EINVAL, "key switch level out of range");
+  const u32 K = kAlpha;
+  const u32 ns = l + K;          // extended slots: q_0..q_{l-1}, P_0..P_3
+  const u32 dn = (l + K - 1) / K;
+  const u64* kbase = key(key_id);
+  const size_t per_lane = (size_t)n * ((size_t)l + (size_t)dn * ns + 2 * ns + 2 * (size_t)l);
+  const size_t budget = (size_t)2 << 30;
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / (per_lane * 8)));
+
+  std::vector<u32> ext_of(ns);
+  for (u32 t = 0; t < ns; ++t) ext_of[t] = t < l ? t : kSpecialBase + (t - l);
+  std::vector<u32> main_off(l), main_ext(l);
+  for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
+
+  u64* ws = alloc(per_lane * B);
+  u64* dc = ws;                                   // [B][l][n]
+  u64* ext = dc + (size_t)B * l * n;              // [B][dn][ns][n]
+  u64* acc = ext + (size_t)B * dn * ns * n;       // [B][2][ns][n]
+  u64* pcv = acc + (size_t)B * 2 * ns * n;        // [B][2][l][n]
+  const size_t ext_ls = (size_t)dn * ns * n, acc_ls = (size_t)2 * ns * n;
+
+  for (u32 l0 = 0; l0 < lanes; l0 += B) {
+    const u32 nb = std::min(B, lanes - l0);
+    const u64* db = d + (size_t)l0 * d_ls;
+    // 1. Intt(l) into the coefficient-domain copy
+    AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(dc, (size_t)l * n * 8, db, d_ls * 8, (size_t)l * n * 8, nb,
+                                       cudaMemcpyDeviceToDevice, stream));
+    ntt(dc, (size_t)l * n, nb, main_off, main_ext, true);
+    // 2. ModUp per digit: exact centred lift of D_j to every other slot, then Ntt
+    for (u32 j = 0; j < dn; ++j) {
+      const u32 lo = j * K, hi = std::min(l, lo + K);
+      std::vector<u32> s_off, s_ext, t_off, t_ext;
+      for (u32 i = lo; i < hi; ++i) { s_off.push_back(i); s_ext.push_back(i); }
+      for (u32 t = 0; t < ns; ++t)
+        if (t < lo || t >= hi) { t_off.push_back(t); t_ext.push_back(ext_of[t]); }
+      u64* ej = ext + (size_t)j * ns * n;
+      basis_convert(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb);
+      ntt(ej, ext_ls, nb, t_off, t_ext, false);
+    }
+    // 3. KeyMul inner product over digits
+    KeyMulIO km;
+    std::memset(&km, 0, sizeof(km));
+    km.ext = ext;
+    km.ext_lane_stride = ext_ls;
+    km.d = db;
+    km.d_lane_stride = d_ls;
+    km.acc = acc;
+    km.acc_lane_stride = acc_ls;
+    km.key = kbase;
+    km.key_slots = key_slots();
+    km.level = l;
+    km.dnum = dn;
+    km.nslots = ns;
+    for (u32 t = 0; t < ns; ++t) {
+      km.slot_ext[t] = ext_of[t];
+      km.slot_key[t] = t < l ? t : chain + (t - l);
+    }
+    AEGIS_CHECK_CUDA(launch_keymul(km, nb, n, d_pc, stream));
+    count();
+    // 4. ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}
+    std::vector<u32> p_off, p_ext;
+    for (u32 c = 0; c < 2; ++c)
+      for (u32 k = 0; k < K; ++k) { p_off.push_back(c * ns + l + k); p_ext.push_back(kSpecialBase + k); }
+    ntt(acc, acc_ls, nb, p_off, p_ext, true);
+    std::vector<u32> ps_off(K), ps_ext(K);
+    for (u32 k = 0; k < K; ++k) { ps_off[k] = l + k; ps_ext[k] = kSpecialBase + k; }
+    // (lane, comp) pairs are uniform "virtual lanes" of stride ns*n / l*n
+    basis_convert(acc, (size_t)ns * n, ps_off, ps_ext, pcv, (size_t)l * n, main_off, main_ext, 2 * nb);
+    ntt(pcv, (size_t)l * n, 2 * nb, main_off, main_ext, false);
+    for (u32 c = 0; c < 2; ++c) {
+      FinishIO f;
+      std::memset(&f, 0, sizeof(f));
+      f.x = acc + (size_t)c * ns * n;
+      f.x_lane = acc_ls;
+      f.y = pcv + (size_t)c * l * n;
+      f.y_lane = (size_t)2 * l * n;
+      f.add = o.add[c] ? o.add[c] + (size_t)l0 * o.add_lane[c] : nullptr;
+      f.add_lane = o.add_lane[c];
+      f.out = o.out[c] + (size_t)l0 * o.out_lane[c];
+      f.out_lane = o.out_lane[c];
+      f.comps = 1;
+      f.limbs = l;
+      for (u32 i = 0; i < l; ++i) {
+        const u64 q = prime(i);
+        u64 P = 1;
+        for (u32 k = 0; k < K; ++k) P = h_mulmod(P, prime(kSpecialBase + k) % q, q);
+        f.ext[i] = i;
+        f.f[i] = h_inv(P, q);
+        f.f_p[i] = h_shoup(f.f[i], q);
+      }
+      AEGIS_CHECK_CUDA(launch_finish(f, nb, n, d_pc, stream));
+      count();
+    }
+  }
+  release(ws);
+}
+
+// ---------------------------------------------------------------------------
+// HE operators
+// ---------------------------------------------------------------------------
+void Context::op_rot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, int offset) {
+  if (level > in.level || level > out.level) throw Error(AEGIS_EINVAL, "rotation level exceeds operand level");
+  // galois element 5^offset mod 2N (rns_math.hpp:142-149)
+  const u64 order = 2ull * n;
+  long long ofs = offset % (long long)n;
+  if (ofs < 0) ofs += n;
+  u64 gk = 1;
+  for (long long i = 0; i < ofs; ++i) gk = (gk * 5) % order;
+  const u64 key_id = 1000u + (u64)(long long)offset;
+  const size_t per_lane = (size_t)2 * level * n;
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)1 << 30) / (per_lane * 8)));
+  u64* tmp = alloc(per_lane * B);
+  const View tv{tmp, B, 2, level};
+  for (u32 l0 = 0; l0 < lanes; l0 += B) {
+    const u32 nb = std::min(B, lanes - l0);
+    // automorphism of both components (eval domain), operand lanes per emit_per_lane
+    if (im.count == lanes) {
+      const LaneMap src_map{im.lane0 + l0, nb};
+      AEGIS_CHECK_CUDA(launch_automorphism(tv, LaneMap{0, nb}, in.view(), src_map, nb, 2, level, log_n, gk, stream));
+      count();
+    } else {
+      for (u32 l = 0; l < nb; ++l) {
+        const u32 il = im.at(l0 + l, lanes);
+        AEGIS_CHECK_CUDA(launch_automorphism(tv, LaneMap{l, 1}, in.view(), LaneMap{il, 1}, 1, 2, level, log_n,
+                                             gk, stream));
+        count();
+      }
+    }
+    KsOut o;
+    o.out[0] = out.view().limb(out_lane + l0, 0, 0, n);
+    o.out[1] = out.view().limb(out_lane + l0, 1, 0, n);
+    o.out_lane[0] = o.out_lane[1] = (size_t)out.comps * out.level * n;
+    o.add[0] = tmp;
+    o.add[1] = nullptr;
+    o.add_lane[0] = o.add_lane[1] = per_lane;
+    keyswitch(tmp + (size_t)level * n, per_lane, nb, level, key_id, o);
+  }
+  release(tmp);
+}
+
+void Context::op_relin(Bundle& b, u32 lane, u32 lanes, u32 level) {
+  if (b.comps < 3) throw Error(AEGIS_ELOGIC, "relinearisation needs a 3-component product");
+  const size_t ls = (size_t)b.comps * b.level * n;
+  KsOut o;
+  o.out[0] = b.view().limb(lane, 0, 0, n);
+  o.out[1] = b.view().limb(lane, 1, 0, n);
+  o.add[0] = o.out[0];
+  o.add[1] = o.out[1];
+  o.out_lane[0] = o.out_lane[1] = o.add_lane[0] = o.add_lane[1] = ls;
+  keyswitch(b.view().limb(lane, 2, 0, n), ls, lanes, level, 0, o);
+}
+
+void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 L) {
+  if (L < 2) throw Error(AEGIS_EINVAL, "level underflow: cannot rescale below level 1");
+  if (im.count != lanes) throw Error(AEGIS_ELOGIC, "rescale operand lanes must match");
+  const u32 m = L - 1;
+  u64* last = alloc((size_t)2 * lanes * n);
+  u64* conv = alloc((size_t)2 * lanes * m * n);
+  // last limb of every (lane, comp) -> [lane][comp][n]
+  AEGIS_CHECK_CUDA(launch_copy(View{last, lanes, 2, 1}, 0, in.view(), im, lanes, 2, 1, L - 1, n, stream));
+  count();
+  ntt(last, n, 2 * lanes, {0}, {L - 1}, true);
+  std::vector<u32> off(m), ext(m);
+  for (u32 i = 0; i < m; ++i) off[i] = ext[i] = i;
+  basis_convert(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * lanes);
+  ntt(conv, (size_t)m * n, 2 * lanes, off, ext, false);
+  FinishIO f;
+  std::memset(&f, 0, sizeof(f));
+  f.x = in.view().limb(im.lane0, 0, 0, n);
+  f.x_lane = (size_t)in.comps * in.level * n;
+  f.x_comp = (size_t)in.level * n;
+  f.y = conv;
+  f.y_lane = (size_t)2 * m * n;
+  f.y_comp = (size_t)m * n;
+  f.out = out.view().limb(out_lane, 0, 0, n);
+  f.out_lane = (size_t)out.comps * out.level * n;
+  f.out_comp = (size_t)out.level * n;
+  f.comps = 2;
+  f.limbs = m;
+  const u64 ql = prime(L - 1);
+  for (u32 i = 0; i < m; ++i) {
+    const u64 q = prime(i);
+    f.ext[i] = i;
+    f.f[i] = h_inv(ql % q, q);
+    f.f_p[i] = h_shoup(f.f[i], q);
+  }
+  AEGIS_CHECK_CUDA(launch_finish(f, lanes, n, d_pc, stream));
+  count();
+  release(last);
+  release(conv);
+}
+
+void Context::op_boot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 L, u32 out_level) {
+  if (im.count != lanes) throw Error(AEGIS_ELOGIC, "boot operand lanes must match");
+  const u32 keep = std::min(L, out_level);
+  AEGIS_CHECK_CUDA(launch_copy(out.view(), out_lane, in.view(), im, lanes, 2, keep, 0, n, stream));
+  count();
+  if (out_level <= L) return;
+  // value-preserving lift: Intt(Q_L) -> exact centred lift -> new limbs -> Ntt
+  u64* xc = alloc((size_t)2 * lanes * L * n);
+  AEGIS_CHECK_CUDA(launch_copy(View{xc, lanes, 2, L}, 0, in.view(), im, lanes, 2, L, 0, n, stream));
+  count();
+  std::vector<u32> soff(L), sext(L);
+  for (u32 i = 0; i < L; ++i) soff[i] = sext[i] = i;
+  ntt(xc, (size_t)L * n, 2 * lanes, soff, sext, true);
+  std::vector<u32> toff, text;
+  for (u32 i = L; i < out_level; ++i) { toff.push_back(i); text.push_back(i); }
+  // virtual lanes (lane, comp): out stride is uniform only when comps == 2
+  if (out.comps == 2) {
+    basis_convert(xc, (size_t)L * n, soff, sext, out.view().limb(out_lane, 0, 0, n), (size_t)out.level * n, toff,
+                  text, 2 * lanes);
+    ntt(out.view().limb(out_lane, 0, 0, n), (size_t)out.level * n, 2 * lanes, toff, text, false);
+  } else {
+    for (u32 c = 0; c < 2; ++c) {
+      basis_convert(xc + (size_t)c * L * n, (size_t)2 * L * n, soff, sext, out.view().limb(out_lane, c, 0, n),
+                    (size_t)out.comps * out.level * n, toff, text, lanes);
+      ntt(out.view().limb(out_lane, c, 0, n), (size_t)out.comps * out.level * n, lanes, toff, text, false);
+    }
+  }
+  release(xc);
+}
+
+void Context::op_cmult(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, LaneMap ma, const Bundle& b,
+                       LaneMap mb, u32 level) {
+  if (out.comps < 3) throw Error(AEGIS_ELOGIC, "CMult output needs 3 components");
+  AEGIS_CHECK_CUDA(launch_cmult(out.view(), out_lane, a.view(), ma, b.view(), mb, lanes, level, n, d_pc, stream));
+  count();
+}
+
+void Context::op_cadd(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, LaneMap ma, const Bundle* b,
+                      LaneMap mb, u32 level, bool acc) {
+  if (!acc && !b) throw Error(AEGIS_ELOGIC, "CAdd needs two operands");
+  AEGIS_CHECK_CUDA(launch_cadd(out.view(), out_lane, a.view(), ma, b ? b->view() : a.view(), mb, acc, lanes, 2,
+                               level, n, d_pc, stream));
+  count();
+}
+
+void Context::op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
+                       u32 x_lanes, u32 wbundle, u32 wlanes, u32 level) {
+  // token groups: in = tg*c_in, out = tg*c_out, w = c_in*c_out
+  u64 tg = 1;
+  while (tg * tg * wlanes < (u64)x_lanes * acc_lanes) ++tg;
+  if (tg * tg * wlanes != (u64)x_lanes * acc_lanes || x_lanes % tg || acc_lanes % tg)
+    throw Error(AEGIS_ELOGIC, "PMult lane shapes inconsistent");
+  const u32 c_in = (u32)(x_lanes / tg), c_out = (u32)(acc_lanes / tg);
+  if ((u64)c_in * c_out != wlanes) throw Error(AEGIS_ELOGIC, "PMult weight lanes inconsistent");
+  const u32 S = (chunk_period == 0 || chunk_period >= acc_lanes) ? 1 : acc_lanes / chunk_period;
+  if (c_out % S) throw Error(AEGIS_ELOGIC, "PMult sub-tensor split inconsistent");
+  const u32 c_sub = c_out / S;
+  u64* rk = alloc((size_t)wlanes * level);
+  AEGIS_CHECK_CUDA(launch_weight_rowkeys(rk, wlanes, level, seed_weight, wbundle, stream));
+  count();
+  for (u32 s = 0; s < S; ++s) {
+    // sub-tensor s occupies acc lanes [s*chunk_period, (s+1)*chunk_period), token-major inside
+    const u32 lane0 = acc_lane + s * (S == 1 ? 0 : chunk_period);
+    AEGIS_CHECK_CUDA(launch_pmult_acc(acc.view(), lane0, x.view(), x_lane, (u32)tg, c_in, c_sub, s * c_sub, c_out,
+                                      level, n, rk, d_pc, stream));
+    count((tg + 3) / 4);
+  }
+  release(rk);
+}
+
+}  // namespace aegis

@@ -1,0 +1,122 @@
+// context.h -- internal C++ state behind the aegis_* C-ABI.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/aegis.h"
+#include "kernels.h"
+#include "ntt.h"
+
+namespace aegis {
+
+// Error carrying an AEGIS_E* code across the C++ layer (mapped at the C-ABI).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define AEGIS_CHECK_CUDA(expr)                                                          \
+  do {                                                                                  \
+    cudaError_t e__ = (expr);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      throw ::aegis::Error(AEGIS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+struct Plan {  // device-resident basis conversion constants
+  ConvPlanDev* dev = nullptr;
+  u64* tables = nullptr;
+  u32 k = 0, m = 0;
+};
+
+struct Bundle {
+  u64* ptr = nullptr;
+  u32 lanes = 0, comps = 0, level = 0;
+  size_t bytes = 0;
+  View view() const { return View{ptr, lanes, comps, level}; }
+};
+
+class Context {
+ public:
+  Context(const aegis_params& p, int device);
+  ~Context();
+
+  // parameters
+  u32 log_n, n, chain, lboot;
+  u64 seed_input, seed_weight, seed_key;
+  int device;
+  cudaStream_t stream = nullptr, comm = nullptr;
+  u64 launches = 0;
+
+  u64 prime(u32 e) const { return primes_.at(e); }
+  u32 post_boot_level() const { return chain - lboot; }
+
+  // device tables
+  PrimeConst* d_pc = nullptr;  // [kNumExt]
+  PrimeTw* d_tw = nullptr;     // [kNumExt]
+  NttScale* d_scale = nullptr; // [kNumExt]
+  u32* d_ident = nullptr;      // identity limb -> ext map [0..kNumExt)
+
+  // memory (stream ordered)
+  u64* alloc(size_t words);
+  void release(void* p);
+  size_t live_bytes = 0, peak_bytes = 0;
+
+  Bundle* new_bundle(u32 lanes, u32 comps, u32 level, bool zero);
+  void free_bundle(Bundle* b);
+
+  // basis conversion plans
+  const Plan& plan(const std::vector<u32>& src_ext, const std::vector<u32>& dst_ext);
+
+  // keys
+  void generate_key(u64 key_id);
+  const u64* key(u64 key_id);
+  u32 key_slots() const { return chain + kAlpha; }
+  u32 key_digits() const { return (chain + kAlpha - 1) / kAlpha; }
+  size_t key_bytes() const { return (size_t)key_digits() * 2 * key_slots() * n * 8; }
+  size_t total_key_bytes() const { return keys_.size() * key_bytes(); }
+
+  // ---- polynomial instructions --------------------------------------------
+  // NTT over rows: lanes x slots, slot_off[i] limbs into the lane, primes[i]
+  void ntt(u64* base, size_t lane_stride, u32 nlanes, const std::vector<u32>& slot_off,
+           const std::vector<u32>& primes, bool inverse);
+  void basis_convert(const u64* src, size_t src_lane_stride, const std::vector<u32>& src_off,
+                     const std::vector<u32>& src_ext, u64* dst, size_t dst_lane_stride,
+                     const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext, u32 lanes);
+  // Hybrid key switch (poly_ir.hpp:219-298) of `lanes` polynomials d (level
+  // limbs each, NTT domain, lane stride d_ls).  out_c = add_c + KS_c(d).
+  struct KsOut {
+    u64* out[2];
+    size_t out_lane[2];
+    const u64* add[2];
+    size_t add_lane[2];
+  };
+  void keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 level, u64 key_id, const KsOut& o);
+
+  // ---- HE operators --------------------------------------------------------
+  void op_rot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, int offset);
+  void op_relin(Bundle& b, u32 lane, u32 lanes, u32 level);
+  void op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level);
+  void op_boot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, u32 out_level);
+  void op_cmult(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, LaneMap ma, const Bundle& b,
+                LaneMap mb, u32 level);
+  void op_cadd(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, LaneMap ma, const Bundle* b,
+               LaneMap mb, u32 level, bool acc);
+  void op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
+                u32 x_lanes, u32 wbundle, u32 wlanes, u32 level);
+
+  void count(u64 k = 1) { launches += k; }
+  std::string last_error;
+
+ private:
+  std::vector<u64> primes_;
+  u64* d_twiddles_ = nullptr;
+  std::map<std::vector<u32>, Plan> plans_;
+  std::map<u64, u64*> keys_;
+  u32* d_key_slot_ext_ = nullptr;  // key slot -> ext prime
+  cudaMemPool_t pool_ = nullptr;
+};
+
+}  // namespace aegis

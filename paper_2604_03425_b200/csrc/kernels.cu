@@ -1,0 +1,480 @@
+// kernels.cu -- elementwise, basis-conversion, key-product and PCMM kernels.
+//
+// All of these are HBM-streaming kernels over [lane][comp][limb][N] u64
+// bundles: a CTA owns a contiguous chunk of one limb row, so
+// every warp access is a 256-byte (or 512-byte with ulonglong2) coalesced
+// segment; per-row constants (prime, lane mapping) are computed once per CTA.
+#include "kernels.h"
+
+namespace aegis {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPerThread = 2;
+constexpr u32 kChunk = kThreads * kPerThread;  // coefficients per CTA
+
+inline u32 chunks_of(u32 n) { return n >= kChunk ? n / kChunk : 1; }
+
+// ---------------------------------------------------------------------------
+// PRNG fills
+// ---------------------------------------------------------------------------
+__global__ void fill_uniform_kernel(View v, u32 comps, u32 limbs, u32 n, u64 seed, u64 tag, u64 a,
+                                    const u32* __restrict__ limb_ext, const PrimeConst* __restrict__ pc,
+                                    u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, lane = rest / comps;
+  const u32 e = limb_ext[lb];
+  const PrimeConst P = pc[e];
+  const u64 rk = row_key(seed, tag, a, lane, comp, lb);
+  u64* dst = v.limb(lane, comp, lb, n);
+  for (u32 x = chunk * kChunk + threadIdx.x; x < n && x < (chunk + 1) * kChunk; x += kThreads)
+    dst[x] = uniform_at(rk, x, P.p, P.shift);
+}
+
+__global__ void fill_key_kernel(u64* key, u32 slots, u32 n, u64 seed, u64 key_id,
+                                const u32* __restrict__ slot_ext, const PrimeConst* __restrict__ pc,
+                                u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 slot = row % slots, rest = row / slots, comp = rest % 2, digit = rest / 2;
+  const u32 e = slot_ext[slot];
+  const PrimeConst P = pc[e];
+  // tag 3: (key_id, digit, comp, ext prime) -- matches oracle key_limb()
+  const u64 rk = row_key(seed, 3, key_id, digit, comp, e);
+  u64* dst = key + (size_t)row * n;
+  for (u32 x = chunk * kChunk + threadIdx.x; x < n && x < (chunk + 1) * kChunk; x += kThreads)
+    dst[x] = uniform_at(rk, x, P.p, P.shift);
+}
+
+// ---------------------------------------------------------------------------
+// Eval-domain automorphism: NTT(auto_k a)[j] = A[brv(((2 brv(j) + 1) k mod 2N - 1) / 2)]
+// ---------------------------------------------------------------------------
+__global__ void automorphism_kernel(View out, LaneMap om, View in, LaneMap im, u32 nlanes, u32 comps,
+                                    u32 limbs, u32 log_n, u64 galois, u32 cpr) {
+  const u32 n = 1u << log_n;
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, l = rest / comps;
+  const u64* src = in.limb(im.at(l, nlanes), comp, lb, n);
+  u64* dst = out.limb(om.at(l, nlanes), comp, lb, n);
+  const u32 mask = 2 * n - 1;
+  const u32 k = (u32)(galois & mask);
+  for (u32 j = chunk * kChunk + threadIdx.x; j < n && j < (chunk + 1) * kChunk; j += kThreads) {
+    const u32 bj = __brev(j) >> (32 - log_n);
+    const u32 e = ((2 * bj + 1) * k) & mask;
+    dst[j] = __ldg(src + (__brev((e - 1) >> 1) >> (32 - log_n)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CMult tensor product and CAdd
+// ---------------------------------------------------------------------------
+__global__ void cmult_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb,
+                             u32 nlanes, u32 limbs, u32 n, const PrimeConst* __restrict__ pc, u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, l = row / limbs;
+  const PrimeConst P = pc[lb];
+  const u32 la = ma.at(l, nlanes), lbn = mb.at(l, nlanes);
+  const u64* a0 = a.limb(la, 0, lb, n);
+  const u64* a1 = a.limb(la, 1, lb, n);
+  const u64* b0 = b.limb(lbn, 0, lb, n);
+  const u64* b1 = b.limb(lbn, 1, lb, n);
+  u64* d0 = out.limb(out_lane0 + l, 0, lb, n);
+  u64* d1 = out.limb(out_lane0 + l, 1, lb, n);
+  u64* d2 = out.limb(out_lane0 + l, 2, lb, n);
+  for (u32 x = chunk * kChunk + threadIdx.x; x < n && x < (chunk + 1) * kChunk; x += kThreads) {
+    const u64 x0 = a0[x], x1 = a1[x], y0 = b0[x], y1 = b1[x];
+    d0[x] = mul_mod(x0, y0, P.p, P.mu104);
+    u128 s = mul_wide(x0, y1);
+    mac(s, x1, y0);
+    d1[x] = reduce104(s, P.p, P.mu104);
+    d2[x] = mul_mod(x1, y1, P.p, P.mu104);
+  }
+}
+
+__global__ void cadd_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, int acc,
+                            u32 nlanes, u32 comps, u32 limbs, u32 n, const PrimeConst* __restrict__ pc,
+                            u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, l = rest / comps;
+  const u64 p = pc[lb].p;
+  const u64* x = a.limb(ma.at(l, nlanes), comp, lb, n);
+  u64* d = out.limb(out_lane0 + l, comp, lb, n);
+  if (acc) {
+    for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
+      d[t] = add_mod(d[t], x[t], p);
+  } else {
+    const u64* y = b.limb(mb.at(l, nlanes), comp, lb, n);
+    for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
+      d[t] = add_mod(x[t], y[t], p);
+  }
+}
+
+__global__ void copy_kernel(View dst, u32 dst_lane0, View src, LaneMap sm, u32 nlanes, u32 comps,
+                            u32 limbs, u32 src_limb0, u32 n, u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, l = rest / comps;
+  const u64* s = src.limb(sm.at(l, nlanes), comp, src_limb0 + lb, n);
+  u64* d = dst.limb(dst_lane0 + l, comp, lb, n);
+  for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads) d[t] = s[t];
+}
+
+__global__ void hash_kernel(View v, u32 comps, u32 limbs, u32 n, unsigned long long* out, u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, lane = rest / comps;
+  const u64* s = v.limb(lane, comp, lb, n);
+  const u64 base = (u64)row * n;  // dense position of (lane, comp, limb, 0)
+  u64 h = 0;
+  for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
+    h += mix64(s[t] + (base + t) * kGold);
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)h);
+}
+
+// ---------------------------------------------------------------------------
+// Exact centred basis conversion
+// ---------------------------------------------------------------------------
+// Rare path: decide v vs v+1 exactly by comparing 2X with (2v+1)B in
+// multiword arithmetic (B odd => never equal).  X = sum xt_i * (B/b_i).
+__device__ __noinline__ u64 tie_resolve(const ConvPlanDev* __restrict__ pl, const u64* __restrict__ hat_big,
+                                        const u64* xt, u32 k, u64 v) {
+  const u32 W = pl->big_words;
+  u64 X[kMaxBigWords + 2];
+  u64 R[kMaxBigWords + 2];
+  for (u32 w = 0; w < W + 2; ++w) X[w] = R[w] = 0;
+  for (u32 i = 0; i < k; ++i) {
+    u64 carry = 0;
+    for (u32 w = 0; w < W; ++w) {
+      const u64 h = hat_big[(size_t)i * W + w];
+      const u64 lo = h * xt[i], hi = __umul64hi(h, xt[i]);
+      u64 s = X[w] + lo;
+      u64 c1 = s < lo;
+      s += carry;
+      c1 += s < carry;
+      X[w] = s;
+      carry = hi + c1;
+    }
+    for (u32 w = W; w < W + 2 && carry; ++w) {
+      X[w] += carry;
+      carry = X[w] < carry;
+    }
+  }
+  // X *= 2
+  u64 top = 0;
+  for (u32 w = 0; w < W + 2; ++w) {
+    const u64 nt = X[w] >> 63;
+    X[w] = (X[w] << 1) | top;
+    top = nt;
+  }
+  // R = (2v+1) * B
+  const u64 mlt = 2 * v + 1;
+  u64 carry = 0;
+  for (u32 w = 0; w < W; ++w) {
+    const u64 lo = pl->b_big[w] * mlt, hi = __umul64hi(pl->b_big[w], mlt);
+    u64 s = lo + carry;
+    carry = hi + (s < lo);
+    R[w] = s;
+  }
+  R[W] = carry;
+  for (int w = (int)W + 1; w >= 0; --w) {
+    if (X[w] != R[w]) return X[w] > R[w] ? v + 1 : v;
+  }
+  return v;  // unreachable (B odd)
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) basis_convert_kernel(const ConvPlanDev* __restrict__ pl,
+                                                            const u64* __restrict__ hat_tab, const ConvIO io,
+                                                            u32 n, u32 kdyn, u32 m) {
+  const u32 k = K > 0 ? (u32)K : kdyn;
+  const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 lane = gid / n, x = gid - lane * n;
+  const u64* src = io.src + (size_t)lane * io.src_lane_stride + x;
+  u64* dst = io.dst + (size_t)lane * io.dst_lane_stride + x;
+  constexpr int KA = K > 0 ? K : kMaxConv;
+  u64 xt[KA];
+  u64 F_lo = 0, F_hi = 0;
+#pragma unroll
+  for (u32 i = 0; i < (u32)KA; ++i) {
+    if (i >= k) break;
+    const u64 b = pl->src_p[i];
+    const u64 t = shoup(src[(size_t)io.src_off[i] * n], pl->hat_inv[i], pl->hat_inv_p[i], b);
+    xt[i] = t;
+    const u64 f = t * pl->w_hi[i] + __umul64hi(t, pl->w_lo[i]);
+    F_lo += f;
+    F_hi += F_lo < f;
+  }
+  // v = round(F / 2^64); ambiguous when the fraction is within 2k ulps below 1/2
+  const u64 half = 1ull << 63;
+  u64 low = F_lo + half;
+  u64 v = F_hi + (low < half);
+  if (low >= (u64)0 - 2ull * k) v = tie_resolve(pl, hat_tab + (size_t)2 * k * m, xt, k, v);
+  const u64* hm = hat_tab;            // [k][m]
+  const u64* hmp = hat_tab + (size_t)k * m;
+  for (u32 t = 0; t < m; ++t) {
+    const u64 d = pl->dst_p[t], mu = pl->dst_mu[t];
+    u64 s = 0;
+#pragma unroll
+    for (u32 i = 0; i < (u32)KA; ++i) {
+      if (i >= k) break;
+      s += shoup_lazy(xt[i], hm[i * m + t], hmp[i * m + t], d);  // < 2d each, k <= 64 terms
+    }
+    u128 ss{s, 0};
+    const u64 r1 = reduce104(ss, d, mu);
+    u128 vv = mul_wide(v, pl->b_mod[t]);
+    const u64 r2 = reduce104(vv, d, mu);
+    dst[(size_t)io.dst_off[t] * n] = sub_mod(r1, r2, d);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Key inner product
+// ---------------------------------------------------------------------------
+__global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeConst* __restrict__ pc,
+                              u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 slot = row % io.nslots, lane = row / io.nslots;
+  const u32 e = io.slot_ext[slot];
+  const PrimeConst P = pc[e];
+  const u32 ks = io.slot_key[slot];
+  const size_t kslot_stride = (size_t)io.key_slots * n;  // per comp
+  const u64* ext = io.ext + (size_t)lane * io.ext_lane_stride + (size_t)slot * n;
+  const u64* dd = io.d + (size_t)lane * io.d_lane_stride + (size_t)slot * n;
+  u64* a0 = io.acc + (size_t)lane * io.acc_lane_stride + (size_t)slot * n;
+  u64* a1 = a0 + (size_t)io.nslots * n;
+  const bool main_slot = slot < io.level;
+  for (u32 x = chunk * kChunk + threadIdx.x; x < n && x < (chunk + 1) * kChunk; x += kThreads) {
+    u128 s0{0, 0}, s1{0, 0};
+    for (u32 j = 0; j < io.dnum; ++j) {
+      const bool own = main_slot && slot >= j * kAlpha && slot < j * kAlpha + kAlpha;
+      const u64 v = own ? dd[x] : ext[(size_t)j * io.nslots * n + x];
+      const u64* kj = io.key + (size_t)j * 2 * kslot_stride + (size_t)ks * n + x;
+      mac(s0, v, __ldg(kj));
+      mac(s1, v, __ldg(kj + kslot_stride));
+    }
+    a0[x] = reduce104(s0, P.p, P.mu104);
+    a1[x] = reduce104(s1, P.p, P.mu104);
+  }
+}
+
+__global__ void finish_kernel(const FinishIO io, u32 n, const PrimeConst* __restrict__ pc, u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % io.limbs, rest = row / io.limbs, comp = rest % io.comps, lane = rest / io.comps;
+  const u64 p = pc[io.ext[lb]].p;
+  const u64 f = io.f[lb], fp = io.f_p[lb];
+  const u64* x = io.x + lane * io.x_lane + comp * io.x_comp + (size_t)lb * n;
+  const u64* y = io.y + lane * io.y_lane + comp * io.y_comp + (size_t)lb * n;
+  const u64* ad = io.add ? io.add + lane * io.add_lane + comp * io.add_comp + (size_t)lb * n : nullptr;
+  u64* o = io.out + lane * io.out_lane + comp * io.out_comp + (size_t)lb * n;
+  for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads) {
+    u64 r = shoup(sub_mod(x[t], y[t], p), f, fp, p);
+    if (ad) r = add_mod(r, ad[t], p);
+    o[t] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bundled PCMM step with in-kernel weights (kGenerate, poly_ir.hpp:57, 310-321)
+// ---------------------------------------------------------------------------
+constexpr u32 kPmTx = 32;      // coefficients per CTA
+constexpr u32 kPmGroups = 8;   // o-groups per CTA (256 threads)
+
+// acc lane for (token group t, output o') is acc_lane0 + t*c_out + o'; the
+// weight lane is ci*w_cout + o_off + o' (o_off/w_cout select one sub-tensor
+// of a chunked accumulator, CtBundle::chunk_period, he_ir.hpp:338).
+template <int TG>
+__global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, View X, u32 x_lane0,
+                                                    u32 c_in, u32 c_out, u32 o_off, u32 w_cout,
+                                                    u32 limbs, u32 n,
+                                                    const u64* __restrict__ rowkeys,
+                                                    const PrimeConst* __restrict__ pc) {
+  extern __shared__ u64 xs[];  // [TG * c_in][2][kPmTx]
+  const u32 tiles = n / kPmTx;
+  const u32 lb = blockIdx.x / tiles;
+  const u32 x0 = (blockIdx.x - lb * tiles) * kPmTx;
+  const PrimeConst P = pc[lb];
+  const u32 nx = TG * c_in;
+  for (u32 e = threadIdx.x; e < nx * 2 * kPmTx; e += blockDim.x) {
+    const u32 xx = e % kPmTx, r = e / kPmTx, comp = r & 1, ln = r >> 1;
+    xs[e] = X.limb(x_lane0 + ln, comp, lb, n)[x0 + xx];
+  }
+  __syncthreads();
+  const u32 xx = threadIdx.x % kPmTx;
+  const u32 og = threadIdx.x / kPmTx;
+  const u64 xi = x0 + xx;
+  for (u32 o = og; o < c_out; o += kPmGroups) {
+    u128 s[TG][2];
+#pragma unroll
+    for (int t = 0; t < TG; ++t) s[t][0] = s[t][1] = u128{0, 0};
+    for (u32 ci = 0; ci < c_in; ++ci) {
+      const u64 rk = rowkeys[(size_t)(ci * w_cout + o_off + o) * limbs + lb];
+      const u64 w = uniform_at(rk, xi, P.p, P.shift);
+#pragma unroll
+      for (int t = 0; t < TG; ++t) {
+        const u32 r = (t * c_in + ci) * 2;
+        mac(s[t][0], xs[r * kPmTx + xx], w);
+        mac(s[t][1], xs[(r + 1) * kPmTx + xx], w);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < TG; ++t)
+#pragma unroll
+      for (int cp = 0; cp < 2; ++cp) {
+        u64* d = acc.limb(acc_lane0 + t * c_out + o, cp, lb, n) + xi;
+        u128 v = s[t][cp];
+        add_to(v, *d);
+        *d = reduce104(v, P.p, P.mu104);
+      }
+  }
+}
+
+__global__ void weight_rowkeys_kernel(u64* out, u32 wlanes, u32 limbs, u64 seed, u64 bundle) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= wlanes * limbs) return;
+  const u32 lane = i / limbs, lb = i - lane * limbs;
+  out[i] = row_key(seed, 2, bundle, lane, 0, lb);  // tag 2: generated weights
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+cudaError_t launch_fill_uniform(View v, u32 lanes, u32 comps, u32 limbs, u32 n, u64 seed, u64 tag,
+                                u64 a, const u32* limb_ext, const PrimeConst* pc, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)lanes * comps * limbs * cpr;
+  if (!g) return cudaSuccess;
+  fill_uniform_kernel<<<(unsigned)g, kThreads, 0, st>>>(v, comps, limbs, n, seed, tag, a, limb_ext, pc, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_key(u64* key, u32 digits, u32 slots, u32 n, u64 seed, u64 key_id,
+                            const u32* slot_ext, const PrimeConst* pc, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)digits * 2 * slots * cpr;
+  fill_key_kernel<<<(unsigned)g, kThreads, 0, st>>>(key, slots, n, seed, key_id, slot_ext, pc, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_automorphism(View out, LaneMap om, View in, LaneMap im, u32 nlanes, u32 comps,
+                                u32 limbs, u32 log_n, u64 galois, cudaStream_t st) {
+  const u32 n = 1u << log_n;
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)nlanes * comps * limbs * cpr;
+  if (!g) return cudaSuccess;
+  automorphism_kernel<<<(unsigned)g, kThreads, 0, st>>>(out, om, in, im, nlanes, comps, limbs, log_n,
+                                                         galois, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cmult(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, u32 nlanes,
+                         u32 limbs, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)nlanes * limbs * cpr;
+  if (!g) return cudaSuccess;
+  cmult_kernel<<<(unsigned)g, kThreads, 0, st>>>(out, out_lane0, a, ma, b, mb, nlanes, limbs, n, pc, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cadd(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, bool acc,
+                        u32 nlanes, u32 comps, u32 limbs, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)nlanes * comps * limbs * cpr;
+  if (!g) return cudaSuccess;
+  cadd_kernel<<<(unsigned)g, kThreads, 0, st>>>(out, out_lane0, a, ma, b, mb, acc ? 1 : 0, nlanes, comps,
+                                                 limbs, n, pc, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(View dst, u32 dst_lane0, View src, LaneMap sm, u32 nlanes, u32 comps, u32 limbs,
+                        u32 src_limb0, u32 n, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)nlanes * comps * limbs * cpr;
+  if (!g) return cudaSuccess;
+  copy_kernel<<<(unsigned)g, kThreads, 0, st>>>(dst, dst_lane0, src, sm, nlanes, comps, limbs, src_limb0, n,
+                                                 cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash(View v, u32 lanes, u32 comps, u32 limbs, u32 n, unsigned long long* out,
+                        cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)lanes * comps * limbs * cpr;
+  if (!g) return cudaSuccess;
+  hash_kernel<<<(unsigned)g, kThreads, 0, st>>>(v, comps, limbs, n, out, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_basis_convert(const ConvPlanDev* plan, const u64* hat_tables, const ConvIO& io,
+                                 u32 lanes, u32 n, u32 k, u32 m, cudaStream_t st) {
+  const size_t total = (size_t)lanes * n;
+  if (!total) return cudaSuccess;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  switch (k) {
+    case 1: basis_convert_kernel<1><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
+    case 2: basis_convert_kernel<2><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
+    case 3: basis_convert_kernel<3><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
+    case 4: basis_convert_kernel<4><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
+    default: basis_convert_kernel<0><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)lanes * io.nslots * cpr;
+  if (!g) return cudaSuccess;
+  keymul_kernel<<<(unsigned)g, kThreads, 0, st>>>(io, lanes, n, pc, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish(const FinishIO& io, u32 lanes, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)lanes * io.comps * io.limbs * cpr;
+  if (!g) return cudaSuccess;
+  finish_kernel<<<(unsigned)g, kThreads, 0, st>>>(io, n, pc, cpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weight_rowkeys(u64* out, u32 wlanes, u32 limbs, u64 seed, u64 bundle, cudaStream_t st) {
+  const u32 total = wlanes * limbs;
+  if (!total) return cudaSuccess;
+  weight_rowkeys_kernel<<<(total + 255) / 256, 256, 0, st>>>(out, wlanes, limbs, seed, bundle);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pmult_acc(View acc, u32 acc_lane0, View x, u32 x_lane0, u32 tg, u32 c_in, u32 c_out,
+                             u32 o_off, u32 w_cout, u32 limbs, u32 n, const u64* w_rowkeys,
+                             const PrimeConst* pc, cudaStream_t st) {
+  if (n < kPmTx) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)tg * c_in * 2 * kPmTx * sizeof(u64);
+  const unsigned grid = limbs * (n / kPmTx);
+  if (!grid) return cudaSuccess;
+#define AEGIS_PM(TGV)                                                                          \
+  case TGV: {                                                                                  \
+    auto kern = pmult_kernel<TGV>;                                                             \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kern<<<grid, kPmTx * kPmGroups, smem, st>>>(acc, acc_lane0, x, x_lane0, c_in, c_out, o_off, w_cout, limbs, n, w_rowkeys, pc); \
+    break;                                                                                     \
+  }
+  switch (tg) {
+    AEGIS_PM(1)
+    AEGIS_PM(2)
+    AEGIS_PM(3)
+    AEGIS_PM(4)
+    default: {
+      // more token groups than the templated cases: process in groups of 4
+      for (u32 t0 = 0; t0 < tg; t0 += 4) {
+        const u32 tt = tg - t0 < 4 ? tg - t0 : 4;
+        cudaError_t e = launch_pmult_acc(acc, acc_lane0 + t0 * c_out, x, x_lane0 + t0 * c_in, tt, c_in,
+                                         c_out, o_off, w_cout, limbs, n, w_rowkeys, pc, st);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+  }
+#undef AEGIS_PM
+  return cudaGetLastError();
+}
+
+}  // namespace aegis

@@ -1,0 +1,57 @@
+"""The C-ABI boundary: library loads, exports every declared symbol, and
+reports errors through codes (no exceptions) -- CPU only, no compute calls."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2604_03425_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "aegis.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(aegis_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = declared()
+    assert len(names) >= 35
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    bound = {s[0] for s in _lib.SIGNATURES}
+    assert set(declared()) == bound
+
+
+def test_ctx_create_rejects_bad_params():
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    p = _lib.AegisParams(16, 35, 3, 14, 1, 2, 3)  # |P| must be 4
+    assert lib.aegis_ctx_create(ctypes.byref(p), 0, ctypes.byref(h)) == _lib.AEGIS_EINVAL
+    assert b"special_prime_count" in lib.aegis_last_error(None)
+    p = _lib.AegisParams(16, 35, 4, 40, 1, 2, 3)  # l_boot > chain (ckks.hpp:45)
+    assert lib.aegis_ctx_create(ctypes.byref(p), 0, ctypes.byref(h)) == _lib.AEGIS_EINVAL
+
+
+def test_null_arguments_are_errors_not_crashes():
+    lib = _lib.load()
+    assert lib.aegis_ctx_create(None, 0, None) == _lib.AEGIS_EINVAL
+    assert lib.aegis_graph_info(None, None, None) == _lib.AEGIS_EINVAL
+    assert lib.aegis_bundle_info(None, None, None, None, None) == _lib.AEGIS_EINVAL
+    assert lib.aegis_graph_dump(None, b"/tmp/x") == _lib.AEGIS_EINVAL
+
+
+def test_graph_key_ids_cover_rotations_and_relin():
+    from paper_2604_03425_b200 import plan_graph
+    g = plan_graph(log_n=16, tokens=128, layers=1)
+    ids = set(int(x) for x in g.key_ids())
+    assert 0 in ids and all(1000 + r in ids for r in range(1, 64))
+    assert len(ids) == 64

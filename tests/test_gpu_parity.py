@@ -1,0 +1,346 @@
+"""GPU parity: every libaegis kernel path vs the CPU oracle, bit-exact on every
+RNS residue (the bar for integer work).  Runs on a B200 via gpurun.
+
+Sizes: toy (N=2^4), small (2^10-2^12) and production (2^16, 2^17) rings.  At
+production size the oracle is only asked for a few lanes / limbs; full-size
+properties (inverse(forward(x)) == x, automorphism group law) cover the rest.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_graph
+from oracle_py import Oracle, hash_bundle
+from tools_params import main_primes, special_primes
+
+pytestmark = pytest.mark.gpu
+
+MP, SP = main_primes(), special_primes()
+
+
+def prime_of(e):
+    return MP[e] if e < 60 else SP[e - 60]
+
+
+_ctx = {}
+_orc = {}
+
+
+def ctx(logn):
+    from paper_2604_03425_b200 import Context
+    if logn not in _ctx:
+        _ctx[logn] = Context(log_n=logn)
+    return _ctx[logn]
+
+
+def orc(logn):
+    if logn not in _orc:
+        _orc[logn] = Oracle(logn)
+    return _orc[logn]
+
+
+def rand_bundle(rng, lanes, comps, level, n):
+    a = np.empty((lanes, comps, level, n), dtype=np.uint64)
+    for lb in range(level):
+        a[:, :, lb, :] = rng.integers(0, prime_of(lb), (lanes, comps, n), dtype=np.uint64)
+    return a
+
+
+def upload(c, arr):
+    b = c.bundle(arr.shape[0], arr.shape[1], arr.shape[2])
+    b.upload(arr)
+    return b
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("logn", [4, 5, 10, 12, 13, 16, 17])
+def test_ntt_forward_inverse(logn):
+    c, o = ctx(logn), orc(logn)
+    rng = np.random.default_rng(logn)
+    level = 3 if logn >= 16 else 6
+    x = rand_bundle(rng, 2, 2, level, 1 << logn)
+    b = upload(c, x)
+    c.ntt(b)
+    f = b.download()
+    for ln in range(2):
+        for cp in range(2):
+            exp = o.ntt(x[ln, cp], list(range(level)))
+            assert (f[ln, cp] == exp).all(), (ln, cp)
+    c.ntt(b, inverse=True)
+    assert (b.download() == x).all()
+
+
+def test_ntt_all_primes_production():
+    """inverse(forward(x)) == x on every one of the 64 primes at N = 2^16, and
+    bit-exact vs the oracle on a sample of them (including the specials)."""
+    c, o = ctx(16), orc(16)
+    n = 1 << 16
+    rng = np.random.default_rng(1)
+    x = rand_bundle(rng, 1, 1, 35, n)
+    b = upload(c, x)
+    c.ntt(b)
+    f = b.download()
+    for lb in (0, 1, 17, 34):
+        assert (f[0, 0, lb] == o.ntt(x[0, 0, lb], [lb])).all()
+    c.ntt(b, inverse=True)
+    assert (b.download() == x).all()
+
+
+def test_ntt_fragment_addressing():
+    """FragSpan-style sub-ranges (poly_ir.hpp:87-99) touch only their limbs."""
+    c, o = ctx(10), orc(10)
+    rng = np.random.default_rng(2)
+    x = rand_bundle(rng, 3, 2, 6, 1 << 10)
+    b = upload(c, x)
+    c.ntt(b, lane=1, lanes=1, lo=2, hi=4)
+    f = b.download()
+    exp = x.copy()
+    for cp in range(2):
+        exp[1, cp, 2:5] = o.ntt(x[1, cp, 2:5], [2, 3, 4])
+    assert (f == exp).all()
+
+
+@pytest.mark.parametrize("logn", [4, 10, 16])
+def test_automorphism(logn):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(3)
+    x = rand_bundle(rng, 2, 2, 4, n)
+    b = upload(c, x)
+    out = c.bundle(2, 2, 4)
+    for off in (1, 5, 63, -1):
+        k = o.L.orc_galois(off, n)
+        c.automorphism(out, b, k)
+        got = out.download()
+        for ln in range(2):
+            for cp in range(2):
+                assert (got[ln, cp] == o.automorphism_eval(x[ln, cp], k)).all()
+
+
+def test_basis_convert_near_ties():
+    c, o = ctx(4), orc(4)
+    n = 16
+    src, dst = [0, 1, 2, 3], [4, 5, 60, 63]
+    B = 1
+    for e in src:
+        B *= prime_of(e)
+    h = (B - 1) // 2
+    vals = [0, 1, B - 1, h, h + 1, h - 1, h + 2, h - 2, B - 2, 12345, B // 3, 2 * B // 3, h + 7, h - 7, 2, 3]
+    x = np.zeros((1, 1, 4, n), dtype=np.uint64)
+    for i, e in enumerate(src):
+        x[0, 0, i] = [v % prime_of(e) for v in vals]
+    bi = upload(c, x)
+    bo = c.bundle(1, 1, 6)
+    c.basis_convert(bo, bi, src, [0, 1, 2, 3], dst, [0, 1, 2, 3])
+    got = bo.download()[0, 0, :4]
+    exp, fb = o.basis_convert(x[0, 0], src, dst)
+    assert fb > 0
+    assert (got == exp).all()
+
+
+@pytest.mark.parametrize("logn,k", [(10, 1), (10, 4), (12, 21), (16, 4)])
+def test_basis_convert_random(logn, k):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(k)
+    src = list(range(k))
+    dst_ext = list(range(k, min(35, k + 10))) + [60, 63]
+    x = rand_bundle(rng, 2, 1, k, n)
+    bi = upload(c, x)
+    bo = c.bundle(2, 1, len(dst_ext))
+    c.basis_convert(bo, bi, src, src, dst_ext, list(range(len(dst_ext))))
+    got = bo.download()
+    for ln in range(2):
+        exp, _ = o.basis_convert(x[ln, 0], src, dst_ext)
+        assert (got[ln, 0] == exp).all()
+
+
+@pytest.mark.parametrize("logn,level", [(4, 1), (4, 5), (10, 3), (10, 9), (12, 17), (16, 6)])
+def test_keyswitch(logn, level):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(level)
+    x = rand_bundle(rng, 2, 2, level, n)
+    bi = upload(c, x)
+    bo = c.bundle(2, 2, level)
+    c.keyswitch(bo, bi, 1, level, 1007)
+    got = bo.download()
+    for ln in range(2):
+        o0, o1 = o.keyswitch(x[ln, 1], level, 1007)
+        assert (got[ln, 0] == o0).all() and (got[ln, 1] == o1).all()
+
+
+@pytest.mark.parametrize("logn,level,offset", [(10, 5, 1), (10, 17, 63), (12, 9, -1), (16, 3, 32)])
+def test_rot(logn, level, offset):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(offset & 0xff)
+    x = rand_bundle(rng, 3, 2, level + 1, n)  # operand one level higher: limb-drop read
+    bi = upload(c, x)
+    bo = c.bundle(3, 2, level)
+    c.rot(bo, bi, offset, level)
+    got = bo.download()
+    for ln in range(3):
+        exp = o.rotate(x[ln, :, :level], level, offset)
+        assert (got[ln] == exp).all(), ln
+
+
+@pytest.mark.parametrize("logn,level", [(10, 4), (10, 16), (16, 3)])
+def test_cmult_relin(logn, level):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(level)
+    a = rand_bundle(rng, 2, 2, level, n)
+    b = rand_bundle(rng, 2, 2, level, n)
+    ba, bb = upload(c, a), upload(c, b)
+    prod = c.bundle(2, 3, level)
+    c.cmult(prod, ba, bb, level)
+    t = prod.download()
+    for ln in range(2):
+        assert (t[ln] == o.cmult(a[ln], b[ln], level)).all()
+    c.relin(prod, level)
+    r = prod.download()
+    for ln in range(2):
+        assert (r[ln, :2] == o.relin(t[ln], level)).all()
+
+
+def test_cmult_lane_maps():
+    """emit_per_lane wrap rule (he_ir.hpp:200-222): b lane = l % count."""
+    c, o = ctx(10), orc(10)
+    n = 1 << 10
+    rng = np.random.default_rng(5)
+    a = rand_bundle(rng, 6, 2, 3, n)
+    b = rand_bundle(rng, 2, 2, 3, n)
+    ba, bb = upload(c, a), upload(c, b)
+    prod = c.bundle(4, 3, 3)
+    c.cmult(prod, ba, bb, 3, lanes=4, a_slice=(2, 4), b_slice=(0, 2))
+    t = prod.download()
+    for ln in range(4):
+        assert (t[ln] == o.cmult(a[2 + ln], b[ln % 2], 3)).all()
+
+
+@pytest.mark.parametrize("logn,level", [(10, 2), (10, 17), (16, 5)])
+def test_rescale(logn, level):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(level)
+    x = rand_bundle(rng, 2, 2, level, n)
+    bi = upload(c, x)
+    bo = c.bundle(2, 2, level - 1)
+    c.rescale(bo, bi, level)
+    got = bo.download()
+    for ln in range(2):
+        assert (got[ln] == o.rescale(x[ln], level)).all()
+
+
+@pytest.mark.parametrize("logn,level,out_level", [(10, 1, 21), (10, 3, 21), (16, 1, 21), (10, 9, 4)])
+def test_boot(logn, level, out_level):
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(level)
+    x = rand_bundle(rng, 2, 2, level, n)
+    bi = upload(c, x)
+    bo = c.bundle(2, 2, out_level)
+    c.boot(bo, bi, level, out_level)
+    got = bo.download()
+    for ln in range(2):
+        assert (got[ln] == o.boot(x[ln], level, out_level)).all()
+
+
+def test_cadd_forms():
+    c = ctx(10)
+    n = 1 << 10
+    rng = np.random.default_rng(8)
+    a = rand_bundle(rng, 4, 2, 3, n)
+    b = rand_bundle(rng, 2, 2, 5, n)
+    ba, bb = upload(c, a), upload(c, b)
+    out = c.bundle(4, 2, 3)
+    c.cadd(out, ba, bb, 3, b_slice=(0, 2))
+    got = out.download()
+    q = np.array([prime_of(i) for i in range(3)], dtype=np.uint64)[None, :, None]
+    for ln in range(4):
+        assert (got[ln] == (a[ln] + b[ln % 2, :, :3]) % q).all()
+    c.cadd(out, bb, None, 3, accumulate=True, a_slice=(0, 2))
+    got2 = out.download()
+    for ln in range(4):
+        assert (got2[ln] == (got[ln] + b[ln % 2, :, :3]) % q).all()
+
+
+@pytest.mark.parametrize("tg,c_in,c_out,chunk", [(1, 3, 4, 0), (2, 2, 3, 0), (2, 3, 6, 6), (5, 2, 2, 0)])
+def test_pmult_acc(tg, c_in, c_out, chunk):
+    """Bundled PCMM step with in-kernel kGenerate weights."""
+    c, o = ctx(10), orc(10)
+    n = 1 << 10
+    level = 3
+    rng = np.random.default_rng(tg * 10 + c_in)
+    x = rand_bundle(rng, tg * c_in, 2, level, n)
+    acc0 = rand_bundle(rng, tg * c_out, 2, level, n)
+    bx, bacc = upload(c, x), upload(c, acc0)
+    wb = 77
+    c.pmult_acc(bacc, bx, wb, c_in * c_out, level, chunk_period=chunk)
+    got = bacc.download()
+    S = 1 if chunk == 0 else (tg * c_out) // chunk
+    c_sub = c_out // S
+    for lb in range(level):
+        p = prime_of(lb)
+        W = [o.weight_limb(wb, lane, lb).astype(object) for lane in range(c_in * c_out)]
+        for t in range(tg):
+            for oo in range(c_out):
+                lane = t * c_out + oo if S == 1 else (oo // c_sub) * chunk + t * c_sub + oo % c_sub
+                for cp in range(2):
+                    s = acc0[lane, cp, lb].astype(object)
+                    for ci in range(c_in):
+                        s = s + x[t * c_in + ci, cp, lb].astype(object) * W[ci * c_out + oo]
+                    assert list(got[lane, cp, lb]) == list(s % p)
+
+
+def test_input_fill_matches_oracle():
+    c, o = ctx(10), orc(10)
+    b = c.bundle(3, 2, 4)
+    b.fill_input(42)
+    got = b.download()
+    assert (got == o.input_bundle(42, 3, 2, 4)).all()
+    assert b.hash() == hash_bundle(got)
+
+
+def test_errors_are_raised_not_crashes():
+    c = ctx(10)
+    b = c.bundle(2, 2, 3)
+    with pytest.raises(ValueError):
+        c.rescale(c.bundle(2, 2, 1), b, 1)  # cannot rescale below level 1
+    with pytest.raises(ValueError):
+        c.rot(c.bundle(2, 2, 3), b, 1, 5)  # level exceeds operand
+    with pytest.raises(ValueError):
+        c.bundle(1, 2, 99)  # level beyond the chain
+
+
+# ---------------------------------------------------------------------------
+# Layer-level parity: full HE-op graphs (reference op sequence) on the GPU vs
+# the oracle's exec_sequential.  Every bundle's content hash at death must match.
+@pytest.mark.parametrize("name,logn", [("ffn_n10_t8", 10), ("block_n10_t8", 10), ("ffn_n11_t32", 11),
+                                       ("block_n11_t32", 11)])
+def test_graph_parity_small(name, logn, golden_dir):
+    path = golden_graph(name, golden_dir)
+    c = ctx(logn)
+    g = c.load_graph(path)
+    h_gpu = g.run(hashes=True)
+    h_cpu = orc(logn).run_graph(path)
+    assert len(h_gpu) == len(h_cpu)
+    bad = [i for i in range(len(h_gpu)) if h_gpu[i] != h_cpu[i]]
+    assert not bad, f"{len(bad)} bundles differ, first {bad[:5]}"
+    assert (h_gpu != 0).sum() > 100
+    # the GPU's own lowering produces the same graph and the same residues
+    g2 = c.graph(kind=1 if name.startswith("ffn") else 0, tokens=int(name.split("_t")[1]))
+    assert (g2.run(hashes=True) == h_gpu).all()
+
+
+@pytest.mark.slow
+def test_graph_parity_config1_production(golden_dir):
+    """Config 1 (FFN 768->3072->768, T=128, N=2^16, l=17..2): a prefix of the op
+    list (first PCMM diagonals) is checked bundle-by-bundle against the oracle."""
+    path = golden_graph("ffn_n16_t128", golden_dir)
+    c = ctx(16)
+    g = c.load_graph(path)
+    ops = 24  # Rot / Encode / PMult for r = 0..7 of ffn1 at level 17
+    h_gpu = g.run(max_ops=ops, hashes=True)
+    h_cpu = orc(16).run_graph(path, max_ops=ops)
+    assert (h_gpu[: len(h_cpu)] == h_cpu).all()
