@@ -144,6 +144,15 @@ int aegis_graph_set_shard(aegis_graph* g, uint32_t tg_lo, uint32_t tg_hi);
  * content hash of bundle b when it dies (0 if never materialised). */
 int aegis_graph_run(aegis_ctx* ctx, aegis_graph* g, int64_t max_ops, uint64_t* hashes,
                     uint64_t nhashes);
+/* Host-buffer execution (the end-to-end path): the graph inputs are read from
+ * `in` (graph-input bundles concatenated in graph order, each
+ * [lane][2][level][N]) and the last op's output bundle is written to `out`.
+ * aegis_graph_io_words gives both sizes; aegis_graph_host_inputs fills a host
+ * buffer with the same synthetic inputs aegis_graph_run generates on device. */
+int aegis_graph_io_words(const aegis_graph* g, uint64_t* in_words, uint64_t* out_words);
+int aegis_graph_host_inputs(aegis_ctx* ctx, const aegis_graph* g, uint64_t* in, uint64_t in_words);
+int aegis_graph_run_host(aegis_ctx* ctx, aegis_graph* g, const uint64_t* in, uint64_t in_words,
+                         uint64_t* out, uint64_t out_words);
 /* key ids the graph needs (for aegis_keys_generate); returns count via *n */
 int aegis_graph_key_ids(const aegis_graph* g, uint64_t* ids, uint32_t cap, uint32_t* n);
 int aegis_graph_free(aegis_graph* g);

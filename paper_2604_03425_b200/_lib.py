@@ -69,6 +69,9 @@ SIGNATURES = [
     ("aegis_graph_info", ctypes.c_int, [vp, u64p, u64p]),
     ("aegis_graph_set_shard", ctypes.c_int, [vp, u32, u32]),
     ("aegis_graph_run", ctypes.c_int, [vp, vp, i64, u64p, u64]),
+    ("aegis_graph_io_words", ctypes.c_int, [vp, u64p, u64p]),
+    ("aegis_graph_host_inputs", ctypes.c_int, [vp, vp, vp, u64]),
+    ("aegis_graph_run_host", ctypes.c_int, [vp, vp, vp, u64, vp, u64]),
     ("aegis_graph_key_ids", ctypes.c_int, [vp, u64p, u32, u32p]),
     ("aegis_graph_free", ctypes.c_int, [vp]),
     ("aegis_graph_peak_bytes", u64, [vp]),

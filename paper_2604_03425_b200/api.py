@@ -269,6 +269,22 @@ class Graph:
         self.ctx._call("aegis_graph_run", self.h, max_ops, None, 0)
         return None
 
+    def io_words(self):
+        i, o = ctypes.c_uint64(), ctypes.c_uint64()
+        self.lib.aegis_graph_io_words(self.h, ctypes.byref(i), ctypes.byref(o))
+        return i.value, o.value
+
+    def fill_host_inputs(self, buf):
+        """buf: any object with data_ptr() (e.g. a pinned torch tensor) or a numpy array."""
+        ptr = buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data
+        words = buf.numel() if hasattr(buf, "numel") else buf.size
+        self.ctx._call("aegis_graph_host_inputs", self.h, ctypes.c_void_p(ptr), words)
+
+    def run_host(self, in_ptr, in_words, out_ptr, out_words):
+        """End-to-end run: inputs H2D from host memory, final bundle D2H."""
+        self.ctx._call("aegis_graph_run_host", self.h, ctypes.c_void_p(in_ptr), in_words,
+                       ctypes.c_void_p(out_ptr), out_words)
+
     def peak_bytes(self):
         return self.lib.aegis_graph_peak_bytes(self.h)
 

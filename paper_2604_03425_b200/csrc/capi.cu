@@ -129,6 +129,13 @@ struct Exec {
   }
   void retire(u32 id) {
     if (!buf[id]) return;
+    if (id == final_bundle && host_out) {
+      const Bundle& b = *buf[id];
+      // first 2 comps of every lane: [lane][2][level][N]
+      AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(host_out, (size_t)2 * b.level * c.n * 8, b.ptr,
+                                         (size_t)b.comps * b.level * c.n * 8, (size_t)2 * b.level * c.n * 8,
+                                         b.lanes, cudaMemcpyDeviceToHost, c.stream));
+    }
     if (d_hash) {
       AEGIS_CHECK_CUDA(aegis::launch_hash(buf[id]->view(), buf[id]->lanes, cur_comps[id], g.bundles[id].level, c.n,
                                           d_hash + id, c.stream));
@@ -138,13 +145,25 @@ struct Exec {
     buf[id] = nullptr;
   }
 
+  const u64* host_in = nullptr;  // graph inputs from host memory (end-to-end path)
+  u64* host_out = nullptr;       // final bundle to host memory
+  u32 final_bundle = 0xffffffffu;
+
   void run(int64_t max_ops) {
+    size_t off = 0;
     for (u32 in : g.graph_inputs) {
       Bundle& b = get(in);
-      AEGIS_CHECK_CUDA(aegis::launch_fill_uniform(b.view(), b.lanes, 2, b.level, c.n, c.seed_input, 1, in, c.d_ident,
-                                                  c.d_pc, c.stream));
-      c.count();
+      if (host_in) {
+        const size_t words = (size_t)b.lanes * 2 * b.level * c.n;
+        AEGIS_CHECK_CUDA(cudaMemcpyAsync(b.ptr, host_in + off, words * 8, cudaMemcpyHostToDevice, c.stream));
+        off += words;
+      } else {
+        AEGIS_CHECK_CUDA(aegis::launch_fill_uniform(b.view(), b.lanes, 2, b.level, c.n, c.seed_input, 1, in,
+                                                    c.d_ident, c.d_pc, c.stream));
+        c.count();
+      }
     }
+    if (host_out && !g.ops.empty()) final_bundle = g.ops.back().out.bundle;
     const int64_t nops = max_ops < 0 ? (int64_t)g.ops.size() : std::min<int64_t>(max_ops, (int64_t)g.ops.size());
     for (int64_t i = 0; i < nops; ++i) {
       const hp::HeOp& op = g.ops[i];
@@ -626,6 +645,60 @@ int aegis_graph_run(aegis_ctx* ctx, aegis_graph* g, int64_t max_ops, uint64_t* h
       for (size_t i = 0; i < nb && i < nhashes; ++i) hashes[i] = h[i];
       c.release(dh);
     }
+    g->peak = c.peak_bytes;
+  });
+}
+int aegis_graph_io_words(const aegis_graph* g, uint64_t* in_words, uint64_t* out_words) {
+  if (!g) return AEGIS_EINVAL;
+  // N is not stored in the graph: infer from the header ("N=<n>")
+  const size_t pos = g->header.find(" N=");
+  const uint64_t n = pos == std::string::npos ? 0 : std::stoull(g->header.substr(pos + 3));
+  uint64_t win = 0;
+  for (u32 b : g->g.graph_inputs) win += (uint64_t)g->g.bundles[b].lanes * 2 * g->g.bundles[b].level * n;
+  uint64_t wout = 0;
+  if (!g->g.ops.empty()) {
+    const hp::CtBundle& fb = g->g.bundles[g->g.ops.back().out.bundle];
+    wout = (uint64_t)fb.lanes * 2 * fb.level * n;
+  }
+  if (in_words) *in_words = win;
+  if (out_words) *out_words = wout;
+  return AEGIS_OK;
+}
+int aegis_graph_host_inputs(aegis_ctx* ctx, const aegis_graph* g, uint64_t* in, uint64_t in_words) {
+  return guard(ctx, [&] {
+    if (!g || !in) throw Error(AEGIS_EINVAL, "null argument");
+    Context& c = *ctx->c;
+    uint64_t need = 0;
+    aegis_graph_io_words(g, &need, nullptr);
+    if (need != in_words) throw Error(AEGIS_EINVAL, "host input size mismatch");
+    size_t off = 0;
+    for (u32 id : g->g.graph_inputs) {
+      const hp::CtBundle& cb = g->g.bundles[id];
+      for (u32 ln = 0; ln < cb.lanes; ++ln)
+        for (u32 cp = 0; cp < 2; ++cp)
+          for (u32 lb = 0; lb < cb.level; ++lb) {
+            const u64 rk = aegis::row_key(c.seed_input, 1, id, ln, cp, lb);
+            const u64 p = c.prime(lb);
+            const u32 sh = (u32)__builtin_clzll(p);
+            for (u32 x = 0; x < c.n; ++x) in[off++] = aegis::uniform_at(rk, x, p, sh);
+          }
+    }
+  });
+}
+int aegis_graph_run_host(aegis_ctx* ctx, aegis_graph* g, const uint64_t* in, uint64_t in_words, uint64_t* out,
+                         uint64_t out_words) {
+  return guard(ctx, [&] {
+    if (!g || !in || !out) throw Error(AEGIS_EINVAL, "null argument");
+    uint64_t wi = 0, wo = 0;
+    aegis_graph_io_words(g, &wi, &wo);
+    if (wi != in_words || wo != out_words) throw Error(AEGIS_EINVAL, "host buffer size mismatch");
+    Context& c = *ctx->c;
+    Exec ex(c, g->g);
+    c.peak_bytes = c.live_bytes;
+    ex.host_in = reinterpret_cast<const u64*>(in);
+    ex.host_out = reinterpret_cast<u64*>(out);
+    ex.run(-1);
+    AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.stream));
     g->peak = c.peak_bytes;
   });
 }

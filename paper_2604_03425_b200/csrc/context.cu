@@ -130,6 +130,7 @@ Context::Context(const aegis_params& prm, int dev) {
     sc[e].n_inv_p = h_shoup(ninv, p);
     sc[e].w1n = h_mulmod(pwi[h_brev(1, (int)log_n)], ninv, p);  // inv[1] * N^{-1}
     sc[e].w1n_p = h_shoup(sc[e].w1n, p);
+    sc[e].mu64 = (u64)((~(u128h)0 >> 64) / p);  // floor((2^64 - 1) / p) == floor(2^64 / p)
   }
   AEGIS_CHECK_CUDA(cudaMalloc(&d_pc, sizeof(PrimeConst) * kNumExt));
   AEGIS_CHECK_CUDA(cudaMalloc(&d_tw, sizeof(PrimeTw) * kNumExt));

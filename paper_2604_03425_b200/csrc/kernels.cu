@@ -208,21 +208,25 @@ __global__ void __launch_bounds__(256) basis_convert_kernel(const ConvPlanDev* _
   u64 low = F_lo + half;
   u64 v = F_hi + (low < half);
   if (low >= (u64)0 - 2ull * k) v = tie_resolve(pl, hat_tab + (size_t)2 * k * m, xt, k, v);
-  const u64* hm = hat_tab;            // [k][m]
-  const u64* hmp = hat_tab + (size_t)k * m;
+  const u64* hm = hat_tab;  // [k][m]: (B/b_i) mod d_t
+  Split xs[KA];
+#pragma unroll
+  for (u32 i = 0; i < (u32)KA; ++i) {
+    if (i >= k) break;
+    xs[i] = split24(xt[i]);
+  }
+  const Split vs = split24(v);
   for (u32 t = 0; t < m; ++t) {
-    const u64 d = pl->dst_p[t], mu = pl->dst_mu[t];
-    u64 s = 0;
+    const u64 d = pl->dst_p[t];
+    // sum_i xt_i [B/b_i]_d + v (d - [B]_d)  ==  x_centred mod d
+    Acc3 s;
 #pragma unroll
     for (u32 i = 0; i < (u32)KA; ++i) {
       if (i >= k) break;
-      s += shoup_lazy(xt[i], hm[i * m + t], hmp[i * m + t], d);  // < 2d each, k <= 64 terms
+      mac24(s, xs[i], split24(__ldg(hm + i * m + t)));
     }
-    u128 ss{s, 0};
-    const u64 r1 = reduce104(ss, d, mu);
-    u128 vv = mul_wide(v, pl->b_mod[t]);
-    const u64 r2 = reduce104(vv, d, mu);
-    dst[(size_t)io.dst_off[t] * n] = sub_mod(r1, r2, d);
+    mac24(s, vs, split24(d - pl->b_mod[t]));
+    dst[(size_t)io.dst_off[t] * n] = acc3_reduce(s, d, pl->dst_mu[t]);
   }
 }
 
@@ -243,16 +247,16 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
   u64* a1 = a0 + (size_t)io.nslots * n;
   const bool main_slot = slot < io.level;
   for (u32 x = chunk * kChunk + threadIdx.x; x < n && x < (chunk + 1) * kChunk; x += kThreads) {
-    u128 s0{0, 0}, s1{0, 0};
+    Acc3 s0, s1;
     for (u32 j = 0; j < io.dnum; ++j) {
       const bool own = main_slot && slot >= j * kAlpha && slot < j * kAlpha + kAlpha;
-      const u64 v = own ? dd[x] : ext[(size_t)j * io.nslots * n + x];
+      const Split v = split24(own ? dd[x] : ext[(size_t)j * io.nslots * n + x]);
       const u64* kj = io.key + (size_t)j * 2 * kslot_stride + (size_t)ks * n + x;
-      mac(s0, v, __ldg(kj));
-      mac(s1, v, __ldg(kj + kslot_stride));
+      mac24(s0, v, split24(__ldg(kj)));
+      mac24(s1, v, split24(__ldg(kj + kslot_stride)));
     }
-    a0[x] = reduce104(s0, P.p, P.mu104);
-    a1[x] = reduce104(s1, P.p, P.mu104);
+    a0[x] = acc3_reduce(s0, P.p, P.mu104);
+    a1[x] = acc3_reduce(s1, P.p, P.mu104);
   }
 }
 
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, Vie
                                                     u32 limbs, u32 n,
                                                     const u64* __restrict__ rowkeys,
                                                     const PrimeConst* __restrict__ pc) {
-  extern __shared__ u64 xs[];  // [TG * c_in][2][kPmTx]
+  extern __shared__ Split xs[];  // [TG * c_in][2][kPmTx], pre-split into 24-bit limbs
   const u32 tiles = n / kPmTx;
   const u32 lb = blockIdx.x / tiles;
   const u32 x0 = (blockIdx.x - lb * tiles) * kPmTx;
@@ -295,24 +299,22 @@ __global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, Vie
   const u32 nx = TG * c_in;
   for (u32 e = threadIdx.x; e < nx * 2 * kPmTx; e += blockDim.x) {
     const u32 xx = e % kPmTx, r = e / kPmTx, comp = r & 1, ln = r >> 1;
-    xs[e] = X.limb(x_lane0 + ln, comp, lb, n)[x0 + xx];
+    xs[e] = split24(X.limb(x_lane0 + ln, comp, lb, n)[x0 + xx]);
   }
   __syncthreads();
   const u32 xx = threadIdx.x % kPmTx;
   const u32 og = threadIdx.x / kPmTx;
   const u64 xi = x0 + xx;
   for (u32 o = og; o < c_out; o += kPmGroups) {
-    u128 s[TG][2];
-#pragma unroll
-    for (int t = 0; t < TG; ++t) s[t][0] = s[t][1] = u128{0, 0};
+    Acc3 s[TG][2];
     for (u32 ci = 0; ci < c_in; ++ci) {
       const u64 rk = rowkeys[(size_t)(ci * w_cout + o_off + o) * limbs + lb];
-      const u64 w = uniform_at(rk, xi, P.p, P.shift);
+      const Split w = split24(uniform_at(rk, xi, P.p, P.shift));
 #pragma unroll
       for (int t = 0; t < TG; ++t) {
         const u32 r = (t * c_in + ci) * 2;
-        mac(s[t][0], xs[r * kPmTx + xx], w);
-        mac(s[t][1], xs[(r + 1) * kPmTx + xx], w);
+        mac24(s[t][0], xs[r * kPmTx + xx], w);
+        mac24(s[t][1], xs[(r + 1) * kPmTx + xx], w);
       }
     }
 #pragma unroll
@@ -320,9 +322,8 @@ __global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, Vie
 #pragma unroll
       for (int cp = 0; cp < 2; ++cp) {
         u64* d = acc.limb(acc_lane0 + t * c_out + o, cp, lb, n) + xi;
-        u128 v = s[t][cp];
-        add_to(v, *d);
-        *d = reduce104(v, P.p, P.mu104);
+        s[t][cp].c0 += *d;
+        *d = acc3_reduce(s[t][cp], P.p, P.mu104);
       }
   }
 }

@@ -54,6 +54,17 @@ __device__ __forceinline__ RowInfo row_info(const NttLaunch& L, u32 row) {
   return r;
 }
 
+// Lazy reduction (Harvey): p < 2^48 leaves 16 bits of headroom in a u64, so
+// butterflies never reduce.  CT: X' = X + T, Y' = X + 2p - T with
+// T = Shoup(Y) in [0, 2p): bounds grow by 2p per stage (< 35p after 17 stages).
+// GS: X' = X + Y, Y' = Shoup(X + B - Y) with B = 2^d p the bound after d
+// stages: the sum path doubles per stage, so the inverse reduces once between
+// its two passes.  Only pass outputs leaving the NTT are made canonical.
+__device__ __forceinline__ u64 reduce_lazy(u64 x, u64 p, u64 mu) {
+  const u64 r = x - __umul64hi(x, mu) * p;  // in [0, 2p)
+  return r >= p ? r - p : r;
+}
+
 // One radix-2^R round of forward CT stages s0 .. s0+R-1 on the sub-problem at sp.
 template <int LOGM>
 __device__ __forceinline__ void ct_round(u64* sp, u32 tau, int s0, u32 t0,
@@ -64,6 +75,7 @@ __device__ __forceinline__ void ct_round(u64* sp, u32 tau, int s0, u32 t0,
   const u32 tau_lo = tau & ((1u << lo_bits) - 1);
   const u32 tau_hi = tau >> lo_bits;
   const u32 base = tau_lo | (tau_hi << (lo_bits + R));
+  const u64 two_p = 2 * p;
   u64 x[1 << R];
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) x[v] = sp[pad_idx(base | ((u32)v << lo_bits))];
@@ -77,21 +89,22 @@ __device__ __forceinline__ void ct_round(u64* sp, u32 tau, int s0, u32 t0,
       const u32 i = (tau_hi << sg) | ((u32)v >> (R - sg));
       const ulonglong2 w = tw[(t0 << s) + i];
       const u64 a = x[v];
-      const u64 b = shoup(x[v + half], w.x, w.y, p);
-      x[v] = add_mod(a, b, p);
-      x[v + half] = sub_mod(a, b, p);
+      const u64 t = shoup_lazy(x[v + half], w.x, w.y, p);
+      x[v] = a + t;
+      x[v + half] = a + two_p - t;
     }
   }
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) sp[pad_idx(base | ((u32)v << lo_bits))] = x[v];
 }
 
-// One radix-2^R round of inverse GS stages s0+R-1 .. s0 (descending).  When
+// One radix-2^R round of inverse GS stages s0+R-1 .. s0 (descending).  `depth`
+// counts GS stages already applied since values were last canonical.  When
 // `last` is set the round contains the global final stage (s == 0 of pass A):
-// both outputs are scaled by N^{-1} there.
+// there N^{-1} is folded into both outputs, which come out canonical.
 template <int LOGM>
 __device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
-                                         const ulonglong2* __restrict__ tw, u64 p,
+                                         const ulonglong2* __restrict__ tw, u64 p, int depth,
                                          bool last, const NttScale& sc) {
   using C = SubCfg<LOGM>;
   constexpr int R = C::R;
@@ -106,6 +119,7 @@ __device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
   for (int sg = R - 1; sg >= 0; --sg) {
     const int s = s0 + sg;
     const int half = 1 << (R - sg - 1);
+    const u64 bound = p << (depth + (R - 1 - sg));
     const bool scale = last && s == 0;
 #pragma unroll
     for (int v = 0; v < (1 << R); ++v) {
@@ -114,12 +128,12 @@ __device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
       const u64 a = x[v], b = x[v + half];
       if (scale) {
         // s == 0: single twiddle inv[1]; fold N^{-1} into both outputs
-        x[v] = shoup(add_mod(a, b, p), sc.n_inv, sc.n_inv_p, p);
-        x[v + half] = shoup(sub_mod(a, b, p), sc.w1n, sc.w1n_p, p);
+        x[v] = shoup(a + b, sc.n_inv, sc.n_inv_p, p);
+        x[v + half] = shoup(a + bound - b, sc.w1n, sc.w1n_p, p);
       } else {
         const ulonglong2 w = tw[(t0 << s) + i];
-        x[v] = add_mod(a, b, p);
-        x[v + half] = shoup(sub_mod(a, b, p), w.x, w.y, p);
+        x[v] = a + b;
+        x[v + half] = shoup_lazy(a + bound - b, w.x, w.y, p);
       }
     }
   }
@@ -128,6 +142,8 @@ __device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
 }
 
 // MODE 0: columns (pass A), MODE 1: contiguous blocks (pass B).
+//   forward : pass A (canonical -> lazy), pass B (lazy -> canonical)
+//   inverse : pass B (canonical -> lazy < 2^kB p), pass A (reduce on load -> canonical)
 template <int LOGM, int MODE, bool INV>
 __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA, int kB,
                                                        int subs_per_cta, int scale_last) {
@@ -138,10 +154,13 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
   const u32 chunk = blockIdx.x - row * ctas_per_row;
   const RowInfo ri = row_info(L, row);
   const PrimeTw pt = L.tw[ri.prime];
+  const NttScale sc = L.scale[ri.prime];
   const ulonglong2* __restrict__ tw = INV ? pt.inv : pt.fwd;
   const u64 p = pt.p;
   const u32 nthreads = blockDim.x;
   const u32 total = subs_per_cta * C::M;
+  const bool reduce_in = INV && MODE == 0;    // lazy intermediate of the inverse
+  const bool reduce_out = !INV && MODE == 1;  // end of the forward transform
 
   // ---- load (coalesced) ----
   if (MODE == 0) {
@@ -150,7 +169,9 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
     const int clog = __ffs(subs_per_cta) - 1;
     for (u32 e = threadIdx.x; e < total; e += nthreads) {
       const u32 c = e & cmask, u = e >> clog;
-      smem[c * C::STRIDE + pad_idx(u)] = ri.ptr[c0 + c + ((size_t)u << kB)];
+      u64 v = ri.ptr[c0 + c + ((size_t)u << kB)];
+      if (reduce_in) v = reduce_lazy(v, p, sc.mu64);
+      smem[c * C::STRIDE + pad_idx(u)] = v;
     }
   } else {
     const size_t off = (size_t)chunk * total;
@@ -175,10 +196,9 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
       }
     }
   } else {
-    const NttScale sc = L.scale[ri.prime];
 #pragma unroll
     for (int rd = C::ROUNDS - 1; rd >= 0; --rd) {
-      gs_round<LOGM>(sp, tau, rd * C::R, t0, tw, p, scale_last && rd == 0, sc);
+      gs_round<LOGM>(sp, tau, rd * C::R, t0, tw, p, (C::ROUNDS - 1 - rd) * C::R, scale_last && rd == 0, sc);
       if (rd > 0) {
         if (C::TPS > 32) __syncthreads(); else __syncwarp();
       }
@@ -199,7 +219,9 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
     const size_t off = (size_t)chunk * total;
     for (u32 e = threadIdx.x; e < total; e += nthreads) {
       const u32 b = e >> LOGM, v = e & (C::M - 1);
-      ri.ptr[off + e] = smem[b * C::STRIDE + pad_idx(v)];
+      u64 x = smem[b * C::STRIDE + pad_idx(v)];
+      if (reduce_out) x = reduce_lazy(x, p, sc.mu64);
+      ri.ptr[off + e] = x;
     }
   }
 }

@@ -12,6 +12,7 @@ struct PrimeTw {
 struct NttScale {
   u64 n_inv, n_inv_p;  // N^{-1} mod p and its Shoup companion (rns_math.hpp:62, 99)
   u64 w1n, w1n_p;      // inv[1] * N^{-1}: last GS stage with the scale folded in
+  u64 mu64;            // floor(2^64 / p): one-step reduction of lazy values
 };
 
 constexpr int kMaxSlots = 96;
