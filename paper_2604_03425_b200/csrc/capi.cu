@@ -113,7 +113,90 @@ struct Exec {
         zero_first[op.out.bundle] = op.accumulate ? 1 : 0;
       }
     }
+    find_hoist_groups();
   }
+
+  // ---- hoisted ModUp across rotations of one source ----------
+  // A group is a run of Rot ops reading the same (bundle, lanes, level) with no
+  // write to that bundle in between (the 63 diagonals of a PCMM / CCMM).
+  struct Group {
+    u32 src, lane0, count, level;
+    int64_t last = -1;
+    u32 size = 0;
+    u64* ext = nullptr;
+    u32 hoisted_lanes = 0;
+    bool prepared = false;
+  };
+  std::vector<Group> groups;
+  std::vector<int> group_of;  // per op (-1 = none)
+
+  void find_hoist_groups() {
+    group_of.assign(g.ops.size(), -1);
+    std::map<u32, int> open;  // src bundle -> open group
+    for (size_t i = 0; i < g.ops.size(); ++i) {
+      const hp::HeOp& op = g.ops[i];
+      if (op.kind == hp::HeOpKind::kRot) {
+        const hp::LaneSlice& s = op.ins[0];
+        auto it = open.find(s.bundle);
+        if (it != open.end()) {
+          Group& gr = groups[it->second];
+          if (gr.lane0 != s.lane || gr.count != s.lane_count || gr.level != op.use_level) open.erase(it);
+        }
+        it = open.find(s.bundle);
+        if (it == open.end()) {
+          groups.push_back(Group{s.bundle, s.lane, s.lane_count, op.use_level});
+          it = open.emplace(s.bundle, (int)groups.size() - 1).first;
+        }
+        Group& gr = groups[it->second];
+        gr.last = (int64_t)i;
+        ++gr.size;
+        group_of[i] = it->second;
+      }
+      if (op.kind != hp::HeOpKind::kEncode) open.erase(op.out.bundle);  // the source is being overwritten
+    }
+  }
+
+  // memory the hoisted ModUp may use: leave room for the rotation outputs and
+  // the key-switch workspace
+  size_t hoist_budget(size_t out_bytes) {
+    size_t fr = 0, total = 0;
+    cudaMemGetInfo(&fr, &total);
+    const size_t reserved = c.live_bytes + c.total_key_bytes() + ((size_t)c.n * 2 * 16 * aegis::kNumExt);
+    const size_t cap = (size_t)(0.92 * (double)total);
+    const size_t margin = out_bytes + ((size_t)6 << 30);
+    return cap > reserved + margin ? cap - reserved - margin : 0;
+  }
+
+  void rot(const hp::HeOp& op, int64_t i, Bundle& in, Bundle& out, u32 lanes, u32 L) {
+    const int gi = group_of[i];
+    if (gi < 0 || groups[gi].size < 2 || op.ins[0].lane_count != lanes || hoist_disabled) {
+      c.op_rot(out, op.out.lane, in, lm(op.ins[0]), lanes, L, op.rot_offset);
+      return;
+    }
+    Group& gr = groups[gi];
+    const size_t per_lane = c.modup_words_per_lane(L);
+    if (!gr.prepared) {
+      gr.prepared = true;
+      const size_t budget = hoist_budget(out.bytes);
+      gr.hoisted_lanes = (u32)std::min<size_t>(lanes, budget / (per_lane * 8));
+      if (gr.hoisted_lanes > 0) {
+        gr.ext = c.alloc(per_lane * gr.hoisted_lanes);
+        c.modup(in.view().limb(op.ins[0].lane, 1, 0, c.n), (size_t)in.comps * in.level * c.n, gr.hoisted_lanes, L,
+                gr.ext);
+      }
+    }
+    const u32 H = gr.hoisted_lanes;
+    if (H > 0)
+      c.op_rot_cached(out, op.out.lane, in, LaneMap{op.ins[0].lane, H}, H, L, op.rot_offset, gr.ext);
+    if (H < lanes)
+      c.op_rot(out, op.out.lane + H, in, LaneMap{op.ins[0].lane + H, lanes - H}, lanes - H, L, op.rot_offset);
+    if (gr.last == i && gr.ext) {
+      c.release(gr.ext);
+      gr.ext = nullptr;
+    }
+  }
+  bool hoist_disabled = false;
+  int64_t cur_op = 0;
 
   Bundle& get(u32 id) {
     if (!buf[id]) {
@@ -167,6 +250,7 @@ struct Exec {
     const int64_t nops = max_ops < 0 ? (int64_t)g.ops.size() : std::min<int64_t>(max_ops, (int64_t)g.ops.size());
     for (int64_t i = 0; i < nops; ++i) {
       const hp::HeOp& op = g.ops[i];
+      cur_op = i;
       step(op);
       std::set<u32> touched{op.out.bundle};
       for (auto& s : op.ins) touched.insert(s.bundle);
@@ -174,6 +258,11 @@ struct Exec {
         if (last_use[b] == i && i + 1 < (int64_t)g.ops.size()) retire(b);
     }
     for (u32 b = 0; b < buf.size(); ++b) retire(b);
+    for (auto& gr : groups)
+      if (gr.ext) {
+        c.release(gr.ext);
+        gr.ext = nullptr;
+      }
   }
 
   static LaneMap lm(const hp::LaneSlice& s) { return LaneMap{s.lane, s.lane_count}; }
@@ -187,7 +276,7 @@ struct Exec {
       case hp::HeOpKind::kRot: {
         Bundle& in = input(op.ins[0]);
         Bundle& out = get(op.out.bundle);
-        c.op_rot(out, op.out.lane, in, lm(op.ins[0]), lanes, L, op.rot_offset);
+        rot(op, cur_op, in, out, lanes, L);
         cur_comps[op.out.bundle] = 2;
         return;
       }
@@ -423,7 +512,27 @@ int aegis_keyswitch(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* in, u
     ko.out_lane[0] = ko.out_lane[1] = (size_t)o.comps * o.level * n;
     ko.add[0] = ko.add[1] = nullptr;
     ko.add_lane[0] = ko.add_lane[1] = 0;
-    ctx->c->keyswitch(i.view().limb(0, comp, 0, n), (size_t)i.comps * i.level * n, i.lanes, level, key_id, ko);
+    Context& c = *ctx->c;
+    if (key_id >= 500) {
+      // rotation keys are stored as key' = auto_{k^-1}(key): KS(d, key) = auto_k(KS(auto_{k^-1}(d), key'))
+      const u64 gk = c.galois_of((int)((long long)key_id - 1000));
+      u64 ginv = 1, b = gk, e = c.n - 1;
+      while (e) {
+        if (e & 1) ginv = (ginv * b) % (2ull * c.n);
+        b = (b * b) % (2ull * c.n);
+        e >>= 1;
+      }
+      u64* tmp2 = c.alloc((size_t)i.lanes * level * n);
+      // component `comp` of every lane: a view based at that component keeps the lane stride
+      aegis::View sv{i.view().limb(0, comp, 0, n), i.lanes, i.comps, i.level};
+      AEGIS_CHECK_CUDA(aegis::launch_automorphism(aegis::View{tmp2, i.lanes, 1, level}, LaneMap{0, i.lanes}, sv,
+                                                  LaneMap{0, i.lanes}, i.lanes, 1, level, c.log_n, ginv, c.stream));
+      c.count();
+      c.keyswitch(tmp2, (size_t)level * n, i.lanes, level, key_id, ko, gk);
+      c.release(tmp2);
+      return;
+    }
+    c.keyswitch(i.view().limb(0, comp, 0, n), (size_t)i.comps * i.level * n, i.lanes, level, key_id, ko);
   });
 }
 

@@ -277,7 +277,33 @@ void Context::generate_key(u64 key_id) {
   }
   AEGIS_CHECK_CUDA(launch_fill_key(k, key_digits(), key_slots(), n, seed_key, key_id, d_key_slot_ext_, d_pc, stream));
   count();
+  if (key_id >= 500) {
+    // Rotation key for offset r = key_id - 1000 is stored pre-permuted by the
+    // inverse automorphism: key'_r = auto_{k^-1}(key_r).  Then
+    //   KS(auto_k(c1)) = auto_k(ModDown(sum_j ModUp(c1)_j * key'_j))
+    // exactly (auto_k is a signed coefficient permutation; the centred lift and
+    // the rounding division commute with it), so the ModUp of c1 no longer
+    // depends on the offset and can be hoisted across rotations.
+    const u64 gk = galois_of((int)((long long)key_id - 1000));
+    const u64 ginv = h_powmod(gk, (u64)n - 1, 2ull * n);  // k^-1 mod 2N (the group has order N)
+    u64* tmp = alloc(words);
+    const u32 rows = key_digits() * 2 * key_slots();
+    AEGIS_CHECK_CUDA(launch_automorphism(View{tmp, rows, 1, 1}, LaneMap{0, rows}, View{k, rows, 1, 1},
+                                         LaneMap{0, rows}, rows, 1, 1, log_n, ginv, stream));
+    count();
+    AEGIS_CHECK_CUDA(cudaMemcpyAsync(k, tmp, words * 8, cudaMemcpyDeviceToDevice, stream));
+    release(tmp);
+  }
   keys_[key_id] = k;
+}
+
+u64 Context::galois_of(int offset) const {  // 5^offset mod 2N (rns_math.hpp:142-149)
+  const u64 order = 2ull * n;
+  long long ofs = offset % (long long)n;
+  if (ofs < 0) ofs += n;
+  u64 gk = 1;
+  for (long long i = 0; i < ofs; ++i) gk = (gk * 5) % order;
+  return gk;
 }
 const u64* Context::key(u64 key_id) {
   auto it = keys_.find(key_id);
@@ -332,83 +358,109 @@ void Context::basis_convert(const u64* src, size_t src_ls, const std::vector<u32
 }
 
 // ---------------------------------------------------------------------------
-// Hybrid key switching.  Lanes are processed in batches whose
-// workspace stays below ks_budget bytes; every kernel of a batch sees all of
-// its lanes, so each key limb is streamed once per batch.
+// Hybrid key switching, split so the ModUp can be hoisted:
+//   modup()   Intt(d) -> per digit exact centred lift to Q_l u P -> Ntt
+//             into ext[lane][digit][slot][n] (own-digit slots are not written:
+//             the key product reads them straight from d)
+//   ks_core() acc_c = sum_j ext_j * key[j][c]  ->  ModDown  ->  finish, where
+//             finish optionally applies the eval-domain automorphism (Rot).
 // ---------------------------------------------------------------------------
-void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id, const KsOut& o) {
-  if (l == 0 || l > chain) throw Error(AEGIS_EINVAL, "key switch level out of range");
-  const u32 K = kAlpha;
-  const u32 ns = l + K;          // extended slots: q_0..q_{l-1}, P_0..P_3
-  const u32 dn = (l + K - 1) / K;
-  const u64* kbase = key(key_id);
-  const size_t per_lane = (size_t)n * ((size_t)l + (size_t)dn * ns + 2 * ns + 2 * (size_t)l);
-  const size_t budget = (size_t)2 << 30;
-  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / (per_lane * 8)));
+Context::KsShape Context::ks_shape(u32 l) const {
+  KsShape s;
+  s.l = l;
+  s.ns = l + kAlpha;
+  s.dn = (l + kAlpha - 1) / kAlpha;
+  return s;
+}
 
-  std::vector<u32> ext_of(ns);
-  for (u32 t = 0; t < ns; ++t) ext_of[t] = t < l ? t : kSpecialBase + (t - l);
+void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
+  if (l == 0 || l > chain) throw Error(AEGIS_EINVAL, "key switch level out of range");
+  const KsShape S = ks_shape(l);
+  const size_t ext_ls = (size_t)S.dn * S.ns * n;
   std::vector<u32> main_off(l), main_ext(l);
   for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
-
-  u64* ws = alloc(per_lane * B);
-  u64* dc = ws;                                   // [B][l][n]
-  u64* ext = dc + (size_t)B * l * n;              // [B][dn][ns][n]
-  u64* acc = ext + (size_t)B * dn * ns * n;       // [B][2][ns][n]
-  u64* pcv = acc + (size_t)B * 2 * ns * n;        // [B][2][l][n]
-  const size_t ext_ls = (size_t)dn * ns * n, acc_ls = (size_t)2 * ns * n;
-
+  const size_t budget = (size_t)1 << 30;
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / ((size_t)l * n * 8)));
+  u64* dc = alloc((size_t)B * l * n);
   for (u32 l0 = 0; l0 < lanes; l0 += B) {
     const u32 nb = std::min(B, lanes - l0);
-    const u64* db = d + (size_t)l0 * d_ls;
-    // 1. Intt(l) into the coefficient-domain copy
-    AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(dc, (size_t)l * n * 8, db, d_ls * 8, (size_t)l * n * 8, nb,
+    AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(dc, (size_t)l * n * 8, d + (size_t)l0 * d_ls, d_ls * 8, (size_t)l * n * 8, nb,
                                        cudaMemcpyDeviceToDevice, stream));
     ntt(dc, (size_t)l * n, nb, main_off, main_ext, true);
-    // 2. ModUp per digit: exact centred lift of D_j to every other slot, then Ntt
-    for (u32 j = 0; j < dn; ++j) {
-      const u32 lo = j * K, hi = std::min(l, lo + K);
+    for (u32 j = 0; j < S.dn; ++j) {
+      const u32 lo = j * kAlpha, hi = std::min(l, lo + kAlpha);
       std::vector<u32> s_off, s_ext, t_off, t_ext;
       for (u32 i = lo; i < hi; ++i) { s_off.push_back(i); s_ext.push_back(i); }
-      for (u32 t = 0; t < ns; ++t)
-        if (t < lo || t >= hi) { t_off.push_back(t); t_ext.push_back(ext_of[t]); }
-      u64* ej = ext + (size_t)j * ns * n;
+      for (u32 t = 0; t < S.ns; ++t)
+        if (t < lo || t >= hi) { t_off.push_back(t); t_ext.push_back(t < l ? t : kSpecialBase + (t - l)); }
+      u64* ej = ext + (size_t)l0 * ext_ls + (size_t)j * S.ns * n;
       basis_convert(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb);
       ntt(ej, ext_ls, nb, t_off, t_ext, false);
     }
-    // 3. KeyMul inner product over digits
-    KeyMulIO km;
-    std::memset(&km, 0, sizeof(km));
-    km.ext = ext;
+  }
+  release(dc);
+}
+
+void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 l, const u64* kbase, u64 galois,
+                      const KsOut& o) {
+  const KsShape S = ks_shape(l);
+  const u32 K = kAlpha, ns = S.ns;
+  const size_t ext_ls = (size_t)S.dn * ns * n, acc_ls = (size_t)2 * ns * n;
+  std::vector<u32> main_off(l), main_ext(l);
+  for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
+  const size_t per_lane = (size_t)n * (2 * ns + 2 * (size_t)l);
+  const size_t budget = (size_t)1 << 30;
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / (per_lane * 8)));
+  u64* acc = alloc(per_lane * B);                 // [B][2][ns][n]
+  u64* pcv = acc + (size_t)B * 2 * ns * n;        // [B][2][l][n]
+  // constants of the finish step: P^{-1} mod q_i
+  FinishIO f;
+  std::memset(&f, 0, sizeof(f));
+  f.comps = 1;
+  f.limbs = l;
+  f.galois = galois;
+  f.log_n = log_n;
+  for (u32 i = 0; i < l; ++i) {
+    const u64 q = prime(i);
+    u64 P = 1;
+    for (u32 k = 0; k < K; ++k) P = h_mulmod(P, prime(kSpecialBase + k) % q, q);
+    f.ext[i] = i;
+    f.f[i] = h_inv(P, q);
+    f.f_p[i] = h_shoup(f.f[i], q);
+  }
+  KeyMulIO km;
+  std::memset(&km, 0, sizeof(km));
+  km.key = kbase;
+  km.key_slots = key_slots();
+  km.level = l;
+  km.dnum = S.dn;
+  km.nslots = ns;
+  for (u32 t = 0; t < ns; ++t) {
+    km.slot_ext[t] = t < l ? t : kSpecialBase + (t - l);
+    km.slot_key[t] = t < l ? t : chain + (t - l);
+  }
+  std::vector<u32> p_off, p_ext, ps_off(K), ps_ext(K);
+  for (u32 c = 0; c < 2; ++c)
+    for (u32 k = 0; k < K; ++k) { p_off.push_back(c * ns + l + k); p_ext.push_back(kSpecialBase + k); }
+  for (u32 k = 0; k < K; ++k) { ps_off[k] = l + k; ps_ext[k] = kSpecialBase + k; }
+
+  for (u32 l0 = 0; l0 < lanes; l0 += B) {
+    const u32 nb = std::min(B, lanes - l0);
+    // KeyMul inner product over digits
+    km.ext = ext + (size_t)l0 * ext_ls;
     km.ext_lane_stride = ext_ls;
-    km.d = db;
+    km.d = d + (size_t)l0 * d_ls;
     km.d_lane_stride = d_ls;
     km.acc = acc;
     km.acc_lane_stride = acc_ls;
-    km.key = kbase;
-    km.key_slots = key_slots();
-    km.level = l;
-    km.dnum = dn;
-    km.nslots = ns;
-    for (u32 t = 0; t < ns; ++t) {
-      km.slot_ext[t] = ext_of[t];
-      km.slot_key[t] = t < l ? t : chain + (t - l);
-    }
     AEGIS_CHECK_CUDA(launch_keymul(km, nb, n, d_pc, stream));
     count();
-    // 4. ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}
-    std::vector<u32> p_off, p_ext;
-    for (u32 c = 0; c < 2; ++c)
-      for (u32 k = 0; k < K; ++k) { p_off.push_back(c * ns + l + k); p_ext.push_back(kSpecialBase + k); }
+    // ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}
     ntt(acc, acc_ls, nb, p_off, p_ext, true);
-    std::vector<u32> ps_off(K), ps_ext(K);
-    for (u32 k = 0; k < K; ++k) { ps_off[k] = l + k; ps_ext[k] = kSpecialBase + k; }
     // (lane, comp) pairs are uniform "virtual lanes" of stride ns*n / l*n
     basis_convert(acc, (size_t)ns * n, ps_off, ps_ext, pcv, (size_t)l * n, main_off, main_ext, 2 * nb);
     ntt(pcv, (size_t)l * n, 2 * nb, main_off, main_ext, false);
     for (u32 c = 0; c < 2; ++c) {
-      FinishIO f;
-      std::memset(&f, 0, sizeof(f));
       f.x = acc + (size_t)c * ns * n;
       f.x_lane = acc_ls;
       f.y = pcv + (size_t)c * l * n;
@@ -417,64 +469,74 @@ void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id,
       f.add_lane = o.add_lane[c];
       f.out = o.out[c] + (size_t)l0 * o.out_lane[c];
       f.out_lane = o.out_lane[c];
-      f.comps = 1;
-      f.limbs = l;
-      for (u32 i = 0; i < l; ++i) {
-        const u64 q = prime(i);
-        u64 P = 1;
-        for (u32 k = 0; k < K; ++k) P = h_mulmod(P, prime(kSpecialBase + k) % q, q);
-        f.ext[i] = i;
-        f.f[i] = h_inv(P, q);
-        f.f_p[i] = h_shoup(f.f[i], q);
-      }
       AEGIS_CHECK_CUDA(launch_finish(f, nb, n, d_pc, stream));
       count();
     }
   }
-  release(ws);
+  release(acc);
+}
+
+void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id, const KsOut& o, u64 galois) {
+  const KsShape S = ks_shape(l);
+  const size_t ext_lane = (size_t)S.dn * S.ns * n;
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)2 << 30) / (ext_lane * 8)));
+  u64* ext = alloc(ext_lane * B);
+  const u64* kbase = key(key_id);
+  for (u32 l0 = 0; l0 < lanes; l0 += B) {
+    const u32 nb = std::min(B, lanes - l0);
+    modup(d + (size_t)l0 * d_ls, d_ls, nb, l, ext);
+    KsOut ob = o;
+    for (int c = 0; c < 2; ++c) {
+      ob.out[c] = o.out[c] + (size_t)l0 * o.out_lane[c];
+      if (o.add[c]) ob.add[c] = o.add[c] + (size_t)l0 * o.add_lane[c];
+    }
+    ks_core(ext, d + (size_t)l0 * d_ls, d_ls, nb, l, kbase, galois, ob);
+  }
+  release(ext);
 }
 
 // ---------------------------------------------------------------------------
 // HE operators
 // ---------------------------------------------------------------------------
 void Context::op_rot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, int offset) {
+  op_rot_cached(out, out_lane, in, im, lanes, level, offset, nullptr);
+}
+
+// Rot_r(c0, c1) = (auto(c0) + KS_0(auto(c1)), KS_1(auto(c1)))
+//              = auto(c0 + MD_0, MD_1),  MD = ModDown(sum_j ModUp(c1)_j key'_r,j)
+// (rotation keys are stored pre-permuted, see generate_key).  `ext` may hold
+// ModUp(c1) of these lanes already (hoisting across the rotations of one
+// source); otherwise it is computed here.
+void Context::op_rot_cached(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level,
+                            int offset, const u64* ext) {
   if (level > in.level || level > out.level) throw Error(AEGIS_EINVAL, "rotation level exceeds operand level");
-  // galois element 5^offset mod 2N (rns_math.hpp:142-149)
-  const u64 order = 2ull * n;
-  long long ofs = offset % (long long)n;
-  if (ofs < 0) ofs += n;
-  u64 gk = 1;
-  for (long long i = 0; i < ofs; ++i) gk = (gk * 5) % order;
+  const u64 gk = galois_of(offset);
   const u64 key_id = 1000u + (u64)(long long)offset;
-  const size_t per_lane = (size_t)2 * level * n;
-  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)1 << 30) / (per_lane * 8)));
-  u64* tmp = alloc(per_lane * B);
-  const View tv{tmp, B, 2, level};
-  for (u32 l0 = 0; l0 < lanes; l0 += B) {
-    const u32 nb = std::min(B, lanes - l0);
-    // automorphism of both components (eval domain), operand lanes per emit_per_lane
-    if (im.count == lanes) {
-      const LaneMap src_map{im.lane0 + l0, nb};
-      AEGIS_CHECK_CUDA(launch_automorphism(tv, LaneMap{0, nb}, in.view(), src_map, nb, 2, level, log_n, gk, stream));
-      count();
-    } else {
-      for (u32 l = 0; l < nb; ++l) {
-        const u32 il = im.at(l0 + l, lanes);
-        AEGIS_CHECK_CUDA(launch_automorphism(tv, LaneMap{l, 1}, in.view(), LaneMap{il, 1}, 1, 2, level, log_n,
-                                             gk, stream));
-        count();
-      }
+  const size_t in_ls = (size_t)in.comps * in.level * n;
+  KsOut o;
+  o.out_lane[0] = o.out_lane[1] = (size_t)out.comps * out.level * n;
+  o.add_lane[0] = o.add_lane[1] = in_ls;
+  o.add[1] = nullptr;
+  if (im.count != lanes) {  // wrapped operand lanes: one lane at a time
+    if (ext) throw Error(AEGIS_ELOGIC, "hoisted rotation needs aligned lanes");
+    for (u32 l = 0; l < lanes; ++l) {
+      const u32 il = im.at(l, lanes);
+      o.out[0] = out.view().limb(out_lane + l, 0, 0, n);
+      o.out[1] = out.view().limb(out_lane + l, 1, 0, n);
+      o.add[0] = in.view().limb(il, 0, 0, n);
+      keyswitch(in.view().limb(il, 1, 0, n), in_ls, 1, level, key_id, o, gk);
     }
-    KsOut o;
-    o.out[0] = out.view().limb(out_lane + l0, 0, 0, n);
-    o.out[1] = out.view().limb(out_lane + l0, 1, 0, n);
-    o.out_lane[0] = o.out_lane[1] = (size_t)out.comps * out.level * n;
-    o.add[0] = tmp;
-    o.add[1] = nullptr;
-    o.add_lane[0] = o.add_lane[1] = per_lane;
-    keyswitch(tmp + (size_t)level * n, per_lane, nb, level, key_id, o);
+    return;
   }
-  release(tmp);
+  o.out[0] = out.view().limb(out_lane, 0, 0, n);
+  o.out[1] = out.view().limb(out_lane, 1, 0, n);
+  o.add[0] = in.view().limb(im.lane0, 0, 0, n);
+  const u64* c1 = in.view().limb(im.lane0, 1, 0, n);
+  if (ext) {
+    ks_core(ext, c1, in_ls, lanes, level, key(key_id), gk, o);
+  } else {
+    keyswitch(c1, in_ls, lanes, level, key_id, o, gk);
+  }
 }
 
 void Context::op_relin(Bundle& b, u32 lane, u32 lanes, u32 level) {

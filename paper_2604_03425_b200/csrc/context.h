@@ -93,10 +93,24 @@ class Context {
     const u64* add[2];
     size_t add_lane[2];
   };
-  void keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 level, u64 key_id, const KsOut& o);
+  // galois != 1 applies the eval-domain automorphism to the result (Rot with
+  // pre-permuted rotation keys).
+  void keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 level, u64 key_id, const KsOut& o, u64 galois = 1);
+  struct KsShape {
+    u32 l, ns, dn;
+  };
+  KsShape ks_shape(u32 l) const;
+  size_t modup_words_per_lane(u32 l) const { return (size_t)ks_shape(l).dn * ks_shape(l).ns * n; }
+  // ext[lane][digit][slot][n] = Ntt(exact lift of Intt(d) digit j to slot t)
+  void modup(const u64* d, size_t d_ls, u32 lanes, u32 level, u64* ext);
+  void ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 level, const u64* key, u64 galois,
+               const KsOut& o);
+  u64 galois_of(int offset) const;
 
   // ---- HE operators --------------------------------------------------------
   void op_rot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, int offset);
+  void op_rot_cached(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, int offset,
+                     const u64* ext);
   void op_relin(Bundle& b, u32 lane, u32 lanes, u32 level);
   void op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level);
   void op_boot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, u32 out_level);

@@ -269,9 +269,15 @@ __global__ void finish_kernel(const FinishIO io, u32 n, const PrimeConst* __rest
   const u64* y = io.y + lane * io.y_lane + comp * io.y_comp + (size_t)lb * n;
   const u64* ad = io.add ? io.add + lane * io.add_lane + comp * io.add_comp + (size_t)lb * n : nullptr;
   u64* o = io.out + lane * io.out_lane + comp * io.out_comp + (size_t)lb * n;
+  const u32 mask = 2 * n - 1, k = (u32)(io.galois & mask);
+  const int sh = 32 - (int)io.log_n;
   for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads) {
-    u64 r = shoup(sub_mod(x[t], y[t], p), f, fp, p);
-    if (ad) r = add_mod(r, ad[t], p);
+    // optional eval-domain automorphism of the result: read position pi(t)
+    // (maps aligned 32-blocks onto aligned 32-blocks, so the gather coalesces)
+    u32 s = t;
+    if (k != 1) s = __brev(((((__brev(t) >> sh) * 2 + 1) * k & mask) - 1) >> 1) >> sh;
+    u64 r = shoup(sub_mod(x[s], y[s], p), f, fp, p);
+    if (ad) r = add_mod(r, ad[s], p);
     o[t] = r;
   }
 }

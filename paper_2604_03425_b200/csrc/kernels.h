@@ -103,6 +103,8 @@ struct FinishIO {
   const u64* add; size_t add_lane, add_comp;  // may be null
   u64* out; size_t out_lane, out_comp;
   u32 comps, limbs;
+  u64 galois;  // 1: none; else out[t] = f(inputs at pi_galois(t)) (eval-domain automorphism)
+  u32 log_n;
   u32 ext[kMaxConv];
   u64 f[kMaxConv], f_p[kMaxConv];
 };
