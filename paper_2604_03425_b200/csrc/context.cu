@@ -9,6 +9,7 @@
 //   boot reset       poly_ir.hpp:355-368
 //   pointwise ops    poly_ir.hpp:192-213
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "context.h"
@@ -89,8 +90,11 @@ Context::Context(const aegis_params& prm, int dev) {
   std::vector<PrimeTw> tw(kNumExt);
   std::vector<NttScale> sc(kNumExt);
   const size_t tab_words = (size_t)n * 2;  // ulonglong2 per entry
-  AEGIS_CHECK_CUDA(cudaMalloc(&d_twiddles_, (size_t)kNumExt * 2 * tab_words * sizeof(u64)));
+  // per prime: int fwd, int inv, f64 fwd, f64 inv
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_twiddles_, (size_t)kNumExt * 4 * tab_words * sizeof(u64)));
   std::vector<u64> hf(tab_words), hi(tab_words), pw(n), pwi(n);
+  std::vector<double> ff(tab_words), fi(tab_words);
+  if (const char* impl = std::getenv("AEGIS_NTT_IMPL")) g_ntt_impl = std::string(impl) == "int" ? kNttInt : kNttF64;
   for (u32 e = 0; e < kNumExt; ++e) {
     const u64 p = primes_[e];
     pc[e].p = p;
@@ -117,13 +121,23 @@ Context::Context(const aegis_params& prm, int dev) {
       hf[2 * i + 1] = h_shoup(pw[r], p);
       hi[2 * i] = pwi[r];
       hi[2 * i + 1] = h_shoup(pwi[r], p);
+      ff[2 * i] = (double)pw[r];
+      ff[2 * i + 1] = (double)pw[r] / (double)p;
+      fi[2 * i] = (double)pwi[r];
+      fi[2 * i + 1] = (double)pwi[r] / (double)p;
     }
-    u64* fdev = d_twiddles_ + (size_t)e * 2 * tab_words;
+    u64* fdev = d_twiddles_ + (size_t)e * 4 * tab_words;
     u64* idev = fdev + tab_words;
+    u64* f64dev = idev + tab_words;
+    u64* i64dev = f64dev + tab_words;
     AEGIS_CHECK_CUDA(cudaMemcpy(fdev, hf.data(), tab_words * 8, cudaMemcpyHostToDevice));
     AEGIS_CHECK_CUDA(cudaMemcpy(idev, hi.data(), tab_words * 8, cudaMemcpyHostToDevice));
+    AEGIS_CHECK_CUDA(cudaMemcpy(f64dev, ff.data(), tab_words * 8, cudaMemcpyHostToDevice));
+    AEGIS_CHECK_CUDA(cudaMemcpy(i64dev, fi.data(), tab_words * 8, cudaMemcpyHostToDevice));
     tw[e].fwd = reinterpret_cast<const ulonglong2*>(fdev);
     tw[e].inv = reinterpret_cast<const ulonglong2*>(idev);
+    tw[e].fwd64 = reinterpret_cast<const double2*>(f64dev);
+    tw[e].inv64 = reinterpret_cast<const double2*>(i64dev);
     tw[e].p = p;
     const u64 ninv = h_inv(n, p);
     sc[e].n_inv = ninv;
@@ -131,6 +145,12 @@ Context::Context(const aegis_params& prm, int dev) {
     sc[e].w1n = h_mulmod(pwi[h_brev(1, (int)log_n)], ninv, p);  // inv[1] * N^{-1}
     sc[e].w1n_p = h_shoup(sc[e].w1n, p);
     sc[e].mu64 = (u64)((~(u128h)0 >> 64) / p);  // floor((2^64 - 1) / p) == floor(2^64 / p)
+    sc[e].pd = (double)p;
+    sc[e].pinv = 1.0 / (double)p;
+    sc[e].n_inv_d = (double)ninv;
+    sc[e].n_inv_wp = (double)ninv / (double)p;
+    sc[e].w1n_d = (double)sc[e].w1n;
+    sc[e].w1n_wp = (double)sc[e].w1n / (double)p;
   }
   AEGIS_CHECK_CUDA(cudaMalloc(&d_pc, sizeof(PrimeConst) * kNumExt));
   AEGIS_CHECK_CUDA(cudaMalloc(&d_tw, sizeof(PrimeTw) * kNumExt));

@@ -5,6 +5,8 @@
 // Gentleman-Sande inverse followed by the N^{-1} scale, which we fold into the
 // last GS stage).  psi and the bit-reversed twiddle tables are the
 // reference's (rns_math.hpp:53-61, 103-117), built on the host in context.cu.
+// Outputs are canonical residues, so any exact butterfly arithmetic gives
+// bit-identical results.
 //
 // B200 design: an N = 2^(kA+kB) transform is two passes over
 // HBM, each a batch of small SMEM-resident sub-transforms:
@@ -16,10 +18,24 @@
 // and runs R butterfly stages per shared-memory round trip (radix-2^R); the
 // SMEM layout pads one word per 16 (+1 per sub-problem) so both the strided
 // and the contiguous round patterns are bank-conflict free.
-// Twiddles are (w, floor(w 2^64/p)) pairs read as one 128-bit load.
+//
+// Two butterfly implementations (g_ntt_impl):
+//   kNttInt -- 64-bit Shoup with lazy (Harvey) reduction.  Bound by the
+//              IMAD pipe: ~13 IMAD-class instructions per butterfly.
+//   kNttF64 -- exact FP64 modular multiply: h = y*w, l = fma(y,w,-h) (exact
+//              product split), q = rint(y * w/p), r = fma(-q,p,h) + l.  With
+//              primes < 2^46 every intermediate is an integer < 2^52, so the
+//              arithmetic is exact; it runs on the DFMA pipe (58.5/clk/SM on
+//              B200) and leaves the integer pipes to addressing.
+// The intermediate between the two passes is lazy (raw u64 or raw double bits);
+// only values leaving the transform are canonicalised.
+#include <type_traits>
+
 #include "ntt.h"
 
 namespace aegis {
+
+int g_ntt_impl = kNttF64;
 
 namespace {
 
@@ -54,29 +70,112 @@ __device__ __forceinline__ RowInfo row_info(const NttLaunch& L, u32 row) {
   return r;
 }
 
-// Lazy reduction (Harvey): p < 2^48 leaves 16 bits of headroom in a u64, so
-// butterflies never reduce.  CT: X' = X + T, Y' = X + 2p - T with
-// T = Shoup(Y) in [0, 2p): bounds grow by 2p per stage (< 35p after 17 stages).
-// GS: X' = X + Y, Y' = Shoup(X + B - Y) with B = 2^d p the bound after d
-// stages: the sum path doubles per stage, so the inverse reduces once between
-// its two passes.  Only pass outputs leaving the NTT are made canonical.
+// ---------------------------------------------------------------------------
+// integer butterflies (lazy Harvey: p < 2^46 leaves >= 18 bits of headroom)
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ u64 reduce_lazy(u64 x, u64 p, u64 mu) {
   const u64 r = x - __umul64hi(x, mu) * p;  // in [0, 2p)
   return r >= p ? r - p : r;
 }
 
+struct IntArith {
+  using T = u64;
+  using Tw = ulonglong2;
+  u64 p, two_p;
+  const NttScale* sc;
+  __device__ __forceinline__ void ct(T& a, T& b, Tw w) const {
+    const u64 t = shoup_lazy(b, w.x, w.y, p);
+    const u64 x = a;
+    a = x + t;
+    b = x + two_p - t;
+  }
+  // `bound` = 2^depth p: both inputs are below it
+  __device__ __forceinline__ void gs(T& a, T& b, Tw w, u64 bound) const {
+    const u64 x = a, y = b;
+    a = x + y;
+    b = shoup_lazy(x + bound - y, w.x, w.y, p);
+  }
+  __device__ __forceinline__ void gs_scale(T& a, T& b, u64 bound) const {
+    const u64 x = a, y = b;
+    a = shoup(x + y, sc->n_inv, sc->n_inv_p, p);
+    b = shoup(x + bound - y, sc->w1n, sc->w1n_p, p);
+  }
+  __device__ __forceinline__ void round_end_gs(T&) const {}
+  __device__ __forceinline__ T load_canon(u64 v) const { return v; }
+  __device__ __forceinline__ T load_lazy(u64 v, bool inverse) const {
+    return inverse ? reduce_lazy(v, p, sc->mu64) : v;
+  }
+  __device__ __forceinline__ u64 store_lazy(T v) const { return v; }
+  __device__ __forceinline__ u64 store_canon(T v, bool already) const {
+    return already ? v : reduce_lazy(v, p, sc->mu64);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// FP64 butterflies: values are integer-valued doubles, |x| < 2^52
+// ---------------------------------------------------------------------------
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double u2d(u64 x) {  // exact for x < 2^52
+  return __longlong_as_double((long long)(x | 0x4330000000000000ULL)) - kTwo52;
+}
+// y * w mod p as a value in about [-p/2 - 1, p/2 + 1]  (exact integer arithmetic)
+__device__ __forceinline__ double mulmod_f64(double y, double w, double wp, double p) {
+  const double h = y * w;
+  const double l = fma(y, w, -h);
+  const double q = rint(y * wp);
+  return fma(-q, p, h) + l;
+}
+__device__ __forceinline__ double reduce_f64(double x, double p, double pinv) {
+  return fma(-rint(x * pinv), p, x);  // |result| <= p/2 + 1
+}
+__device__ __forceinline__ u64 canon_f64(double x, double p, double pinv) {
+  double r = reduce_f64(x, p, pinv);
+  r = r < 0.0 ? r + p : r;
+  r = r >= p ? r - p : r;
+  return (u64)__double_as_longlong(r + kTwo52) & 0xFFFFFFFFFFFFFULL;
+}
+
+struct F64Arith {
+  using T = double;
+  using Tw = double2;
+  double p, pinv;
+  const NttScale* sc;
+  __device__ __forceinline__ void ct(T& a, T& b, Tw w) const {
+    const double t = mulmod_f64(b, w.x, w.y, p);
+    const double x = a;
+    a = x + t;
+    b = x - t;
+  }
+  __device__ __forceinline__ void gs(T& a, T& b, Tw w, u64) const {
+    const double x = a, y = b;
+    a = x + y;
+    b = mulmod_f64(x - y, w.x, w.y, p);
+  }
+  __device__ __forceinline__ void gs_scale(T& a, T& b, u64) const {
+    const double x = a, y = b;
+    a = mulmod_f64(x + y, sc->n_inv_d, sc->n_inv_wp, p);
+    b = mulmod_f64(x - y, sc->w1n_d, sc->w1n_wp, p);
+  }
+  // the GS sum path doubles per stage: fold back below p once per round
+  __device__ __forceinline__ void round_end_gs(T& x) const { x = reduce_f64(x, p, pinv); }
+  __device__ __forceinline__ T load_canon(u64 v) const { return u2d(v); }
+  __device__ __forceinline__ T load_lazy(u64 v, bool) const { return __longlong_as_double((long long)v); }
+  __device__ __forceinline__ u64 store_lazy(T v) const { return (u64)__double_as_longlong(v); }
+  __device__ __forceinline__ u64 store_canon(T v, bool) const { return canon_f64(v, p, pinv); }
+};
+
 // One radix-2^R round of forward CT stages s0 .. s0+R-1 on the sub-problem at sp.
-template <int LOGM>
-__device__ __forceinline__ void ct_round(u64* sp, u32 tau, int s0, u32 t0,
-                                         const ulonglong2* __restrict__ tw, u64 p) {
+template <int LOGM, class A>
+__device__ __forceinline__ void ct_round(typename A::T* sp, u32 tau, int s0, u32 t0,
+                                         const typename A::Tw* __restrict__ tw, const A& ar) {
   using C = SubCfg<LOGM>;
   constexpr int R = C::R;
   const int lo_bits = LOGM - s0 - R;
   const u32 tau_lo = tau & ((1u << lo_bits) - 1);
   const u32 tau_hi = tau >> lo_bits;
   const u32 base = tau_lo | (tau_hi << (lo_bits + R));
-  const u64 two_p = 2 * p;
-  u64 x[1 << R];
+  typename A::T x[1 << R];
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) x[v] = sp[pad_idx(base | ((u32)v << lo_bits))];
 #pragma unroll
@@ -87,11 +186,7 @@ __device__ __forceinline__ void ct_round(u64* sp, u32 tau, int s0, u32 t0,
     for (int v = 0; v < (1 << R); ++v) {
       if (v & half) continue;
       const u32 i = (tau_hi << sg) | ((u32)v >> (R - sg));
-      const ulonglong2 w = tw[(t0 << s) + i];
-      const u64 a = x[v];
-      const u64 t = shoup_lazy(x[v + half], w.x, w.y, p);
-      x[v] = a + t;
-      x[v + half] = a + two_p - t;
+      ar.ct(x[v], x[v + half], tw[(t0 << s) + i]);
     }
   }
 #pragma unroll
@@ -99,20 +194,20 @@ __device__ __forceinline__ void ct_round(u64* sp, u32 tau, int s0, u32 t0,
 }
 
 // One radix-2^R round of inverse GS stages s0+R-1 .. s0 (descending).  `depth`
-// counts GS stages already applied since values were last canonical.  When
+// counts GS stages since values were last reduced (integer bounds).  When
 // `last` is set the round contains the global final stage (s == 0 of pass A):
-// there N^{-1} is folded into both outputs, which come out canonical.
-template <int LOGM>
-__device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
-                                         const ulonglong2* __restrict__ tw, u64 p, int depth,
-                                         bool last, const NttScale& sc) {
+// there N^{-1} is folded into both outputs.
+template <int LOGM, class A>
+__device__ __forceinline__ void gs_round(typename A::T* sp, u32 tau, int s0, u32 t0,
+                                         const typename A::Tw* __restrict__ tw, const A& ar, int depth,
+                                         bool last, u64 p) {
   using C = SubCfg<LOGM>;
   constexpr int R = C::R;
   const int lo_bits = LOGM - s0 - R;
   const u32 tau_lo = tau & ((1u << lo_bits) - 1);
   const u32 tau_hi = tau >> lo_bits;
   const u32 base = tau_lo | (tau_hi << (lo_bits + R));
-  u64 x[1 << R];
+  typename A::T x[1 << R];
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) x[v] = sp[pad_idx(base | ((u32)v << lo_bits))];
 #pragma unroll
@@ -125,17 +220,13 @@ __device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
     for (int v = 0; v < (1 << R); ++v) {
       if (v & half) continue;
       const u32 i = (tau_hi << sg) | ((u32)v >> (R - sg));
-      const u64 a = x[v], b = x[v + half];
-      if (scale) {
-        // s == 0: single twiddle inv[1]; fold N^{-1} into both outputs
-        x[v] = shoup(a + b, sc.n_inv, sc.n_inv_p, p);
-        x[v + half] = shoup(a + bound - b, sc.w1n, sc.w1n_p, p);
-      } else {
-        const ulonglong2 w = tw[(t0 << s) + i];
-        x[v] = a + b;
-        x[v + half] = shoup_lazy(a + bound - b, w.x, w.y, p);
-      }
+      if (scale) ar.gs_scale(x[v], x[v + half], bound);
+      else ar.gs(x[v], x[v + half], tw[(t0 << s) + i], bound);
     }
+  }
+  if (!last) {
+#pragma unroll
+    for (int v = 0; v < (1 << R); ++v) ar.round_end_gs(x[v]);
   }
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) sp[pad_idx(base | ((u32)v << lo_bits))] = x[v];
@@ -143,24 +234,37 @@ __device__ __forceinline__ void gs_round(u64* sp, u32 tau, int s0, u32 t0,
 
 // MODE 0: columns (pass A), MODE 1: contiguous blocks (pass B).
 //   forward : pass A (canonical -> lazy), pass B (lazy -> canonical)
-//   inverse : pass B (canonical -> lazy < 2^kB p), pass A (reduce on load -> canonical)
-template <int LOGM, int MODE, bool INV>
+//   inverse : pass B (canonical -> lazy), pass A (lazy -> canonical)
+template <int LOGM, int MODE, bool INV, int IMPL>
 __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA, int kB,
                                                        int subs_per_cta, int scale_last) {
   using C = SubCfg<LOGM>;
-  extern __shared__ u64 smem[];
+  using A = typename std::conditional<IMPL == kNttF64, F64Arith, IntArith>::type;
+  using T = typename A::T;
+  extern __shared__ u64 smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
   const u32 ctas_per_row = MODE == 0 ? (1u << kB) / subs_per_cta : (1u << kA) / subs_per_cta;
   const u32 row = blockIdx.x / ctas_per_row;
   const u32 chunk = blockIdx.x - row * ctas_per_row;
   const RowInfo ri = row_info(L, row);
   const PrimeTw pt = L.tw[ri.prime];
-  const NttScale sc = L.scale[ri.prime];
-  const ulonglong2* __restrict__ tw = INV ? pt.inv : pt.fwd;
-  const u64 p = pt.p;
+  const NttScale* sc = L.scale + ri.prime;
+  A ar;
+  if constexpr (IMPL == kNttF64) {
+    ar.p = sc->pd;
+    ar.pinv = sc->pinv;
+  } else {
+    ar.p = pt.p;
+    ar.two_p = 2 * pt.p;
+  }
+  ar.sc = sc;
+  const typename A::Tw* __restrict__ tw;
+  if constexpr (IMPL == kNttF64) tw = INV ? pt.inv64 : pt.fwd64;
+  else tw = INV ? pt.inv : pt.fwd;
   const u32 nthreads = blockDim.x;
   const u32 total = subs_per_cta * C::M;
-  const bool reduce_in = INV && MODE == 0;    // lazy intermediate of the inverse
-  const bool reduce_out = !INV && MODE == 1;  // end of the forward transform
+  // which side of this pass is canonical (the other is the lazy intermediate)
+  const bool in_canon = (!INV && MODE == 0) || (INV && MODE == 1);
 
   // ---- load (coalesced) ----
   if (MODE == 0) {
@@ -169,28 +273,28 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
     const int clog = __ffs(subs_per_cta) - 1;
     for (u32 e = threadIdx.x; e < total; e += nthreads) {
       const u32 c = e & cmask, u = e >> clog;
-      u64 v = ri.ptr[c0 + c + ((size_t)u << kB)];
-      if (reduce_in) v = reduce_lazy(v, p, sc.mu64);
-      smem[c * C::STRIDE + pad_idx(u)] = v;
+      const u64 v = ri.ptr[c0 + c + ((size_t)u << kB)];
+      smem[c * C::STRIDE + pad_idx(u)] = in_canon ? ar.load_canon(v) : ar.load_lazy(v, INV);
     }
   } else {
     const size_t off = (size_t)chunk * total;
     for (u32 e = threadIdx.x; e < total; e += nthreads) {
       const u32 b = e >> LOGM, v = e & (C::M - 1);
-      smem[b * C::STRIDE + pad_idx(v)] = ri.ptr[off + e];
+      const u64 x = ri.ptr[off + e];
+      smem[b * C::STRIDE + pad_idx(v)] = in_canon ? ar.load_canon(x) : ar.load_lazy(x, INV);
     }
   }
   __syncthreads();
 
   const u32 sub = threadIdx.x / C::TPS;
   const u32 tau = threadIdx.x - sub * C::TPS;
-  u64* sp = smem + sub * C::STRIDE;
+  T* sp = smem + sub * C::STRIDE;
   const u32 t0 = MODE == 0 ? 1u : (1u << kA) + chunk * subs_per_cta + sub;
   // block = subs_per_cta * TPS threads exactly, so every thread owns work
   if (!INV) {
 #pragma unroll
     for (int rd = 0; rd < C::ROUNDS; ++rd) {
-      ct_round<LOGM>(sp, tau, rd * C::R, t0, tw, p);
+      ct_round<LOGM, A>(sp, tau, rd * C::R, t0, tw, ar);
       if (rd + 1 < C::ROUNDS) {
         if (C::TPS > 32) __syncthreads(); else __syncwarp();
       }
@@ -198,7 +302,7 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
   } else {
 #pragma unroll
     for (int rd = C::ROUNDS - 1; rd >= 0; --rd) {
-      gs_round<LOGM>(sp, tau, rd * C::R, t0, tw, p, (C::ROUNDS - 1 - rd) * C::R, scale_last && rd == 0, sc);
+      gs_round<LOGM, A>(sp, tau, rd * C::R, t0, tw, ar, (C::ROUNDS - 1 - rd) * C::R, scale_last && rd == 0, pt.p);
       if (rd > 0) {
         if (C::TPS > 32) __syncthreads(); else __syncwarp();
       }
@@ -207,28 +311,31 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA
   __syncthreads();
 
   // ---- store (coalesced) ----
+  // canonical output side: forward pass B and inverse pass A (the integer
+  // inverse is already canonical after the scaled stage)
+  const bool out_canon = !in_canon;
+  const bool int_already = INV;
   if (MODE == 0) {
     const u32 c0 = chunk * subs_per_cta;
     const u32 cmask = subs_per_cta - 1;
     const int clog = __ffs(subs_per_cta) - 1;
     for (u32 e = threadIdx.x; e < total; e += nthreads) {
       const u32 c = e & cmask, u = e >> clog;
-      ri.ptr[c0 + c + ((size_t)u << kB)] = smem[c * C::STRIDE + pad_idx(u)];
+      const T x = smem[c * C::STRIDE + pad_idx(u)];
+      ri.ptr[c0 + c + ((size_t)u << kB)] = out_canon ? ar.store_canon(x, int_already) : ar.store_lazy(x);
     }
   } else {
     const size_t off = (size_t)chunk * total;
     for (u32 e = threadIdx.x; e < total; e += nthreads) {
       const u32 b = e >> LOGM, v = e & (C::M - 1);
-      u64 x = smem[b * C::STRIDE + pad_idx(v)];
-      if (reduce_out) x = reduce_lazy(x, p, sc.mu64);
-      ri.ptr[off + e] = x;
+      const T x = smem[b * C::STRIDE + pad_idx(v)];
+      ri.ptr[off + e] = out_canon ? ar.store_canon(x, int_already) : ar.store_lazy(x);
     }
   }
 }
 
-template <int LOGM, int MODE, bool INV>
-cudaError_t launch_pass(const NttLaunch& L, int kA, int kB, u32 rows, int scale_last,
-                        cudaStream_t st) {
+template <int LOGM, int MODE, bool INV, int IMPL>
+cudaError_t launch_pass(const NttLaunch& L, int kA, int kB, u32 rows, int scale_last, cudaStream_t st) {
   using C = SubCfg<LOGM>;
   const int nsub_total = MODE == 0 ? (1 << kB) : (1 << kA);
   int subs = 256 / C::TPS;
@@ -236,7 +343,7 @@ cudaError_t launch_pass(const NttLaunch& L, int kA, int kB, u32 rows, int scale_
   if (subs < 1) subs = 1;
   const u32 ctas_per_row = nsub_total / subs;
   const size_t smem = (size_t)subs * C::STRIDE * sizeof(u64);
-  auto kern = ntt_pass_kernel<LOGM, MODE, INV>;
+  auto kern = ntt_pass_kernel<LOGM, MODE, INV, IMPL>;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
@@ -246,38 +353,43 @@ cudaError_t launch_pass(const NttLaunch& L, int kA, int kB, u32 rows, int scale_
   return cudaGetLastError();
 }
 
-template <int MODE, bool INV>
+template <int MODE, bool INV, int IMPL>
 cudaError_t dispatch_pass(int logm, const NttLaunch& L, int kA, int kB, u32 rows, int scale_last,
                           cudaStream_t st) {
   switch (logm) {
-    case 1: return launch_pass<1, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 2: return launch_pass<2, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 3: return launch_pass<3, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 4: return launch_pass<4, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 5: return launch_pass<5, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 6: return launch_pass<6, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 7: return launch_pass<7, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 8: return launch_pass<8, MODE, INV>(L, kA, kB, rows, scale_last, st);
-    case 9: return launch_pass<9, MODE, INV>(L, kA, kB, rows, scale_last, st);
+    case 1: return launch_pass<1, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 2: return launch_pass<2, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 3: return launch_pass<3, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 4: return launch_pass<4, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 5: return launch_pass<5, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 6: return launch_pass<6, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 7: return launch_pass<7, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 8: return launch_pass<8, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
+    case 9: return launch_pass<9, MODE, INV, IMPL>(L, kA, kB, rows, scale_last, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+template <int IMPL>
+cudaError_t run_impl(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st) {
+  const u32 rows = L.nlanes * L.nslots;
+  const int kA = log_n / 2, kB = log_n - kA;
+  cudaError_t e;
+  if (!inverse) {
+    e = dispatch_pass<0, false, IMPL>(kA, L, kA, kB, rows, 0, st);
+    if (e != cudaSuccess) return e;
+    return dispatch_pass<1, false, IMPL>(kB, L, kA, kB, rows, 0, st);
+  }
+  e = dispatch_pass<1, true, IMPL>(kB, L, kA, kB, rows, 0, st);
+  if (e != cudaSuccess) return e;
+  return dispatch_pass<0, true, IMPL>(kA, L, kA, kB, rows, 1, st);
 }
 
 }  // namespace
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st) {
-  const u32 rows = L.nlanes * L.nslots;
-  if (rows == 0) return cudaSuccess;
-  const int kA = log_n / 2, kB = log_n - kA;
-  cudaError_t e;
-  if (!inverse) {
-    e = dispatch_pass<0, false>(kA, L, kA, kB, rows, 0, st);
-    if (e != cudaSuccess) return e;
-    return dispatch_pass<1, false>(kB, L, kA, kB, rows, 0, st);
-  }
-  e = dispatch_pass<1, true>(kB, L, kA, kB, rows, 0, st);
-  if (e != cudaSuccess) return e;
-  return dispatch_pass<0, true>(kA, L, kA, kB, rows, 1, st);
+  if (L.nlanes * L.nslots == 0) return cudaSuccess;
+  return g_ntt_impl == kNttF64 ? run_impl<kNttF64>(L, log_n, inverse, st) : run_impl<kNttInt>(L, log_n, inverse, st);
 }
 
 }  // namespace aegis

@@ -7,13 +7,21 @@ namespace aegis {
 struct PrimeTw {
   const ulonglong2* fwd;  // N entries (w, shoup(w)) : psi^brv(i)   (rns_math.hpp:59)
   const ulonglong2* inv;  // N entries : psi^-brv(i)                 (rns_math.hpp:60)
+  const double2* fwd64;   // N entries (w, w/p) as doubles (FP64 butterflies)
+  const double2* inv64;
   u64 p;
 };
 struct NttScale {
   u64 n_inv, n_inv_p;  // N^{-1} mod p and its Shoup companion (rns_math.hpp:62, 99)
   u64 w1n, w1n_p;      // inv[1] * N^{-1}: last GS stage with the scale folded in
   u64 mu64;            // floor(2^64 / p): one-step reduction of lazy values
+  double pd, pinv;     // p and 1/p as doubles
+  double n_inv_d, n_inv_wp, w1n_d, w1n_wp;  // FP64 forms of the scale constants
 };
+
+// Butterfly arithmetic of the NTT passes.
+enum NttImpl : int { kNttInt = 0, kNttF64 = 1 };
+extern int g_ntt_impl;  // selected at context creation (AEGIS_NTT_IMPL=int|f64)
 
 constexpr int kMaxSlots = 96;
 

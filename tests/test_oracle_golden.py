@@ -57,7 +57,7 @@ def test_prime_chain():
     allp = MP + SP
     assert len(MP) == 60 and len(SP) == 4 and len(set(allp)) == 64
     for p in allp:
-        assert is_prime(p) and (p - 1) % (1 << 18) == 0 and p < (1 << 48)
+        assert is_prime(p) and (p - 1) % (1 << 18) == 0 and p < (1 << 46)
     # log2(Q_35 * P) close to the paper's 1661 bits
     q = 1
     for p in MP[:35] + SP:
