@@ -174,9 +174,12 @@ def run_aegis(args):
     c = Context(log_n=N_LOG, device=local)
     g = c.graph(kind=0, tokens=args.tokens, layers=args.layers)
     tg_total = -(-args.tokens // ((1 << N_LOG) // 2 // 64))
-    lo, hi = shard_range(tg_total, rank, ws)
     if ws > 1:
-        g.set_shard(lo, hi)
+        from paper_2604_03425_b200.dist import make_reducer, token_group_comms
+        g.set_shard(ws, rank)
+        groups, m = token_group_comms(ws, tg_total)
+        if m > 1:
+            g.set_reducer(make_reducer(groups, rank % m))
     c.keys_generate(g.key_ids())
     c.sync()
     st = torch.cuda.ExternalStream(c.stream)
@@ -257,7 +260,8 @@ def end_to_end(c, g, args, st, barrier):
         g.run_host(hin.data_ptr(), in_words, hout.data_ptr(), out_words)
     e1.record(st)
     e1.synchronize()
-    return e0.elapsed_time(e1) / steps, in_words * 8, out_words * 8
+    h2d, d2h = g.io_bytes()  # bytes actually copied by the last run (owned lanes only when sharded)
+    return e0.elapsed_time(e1) / steps, h2d, d2h
 
 
 def ntt_roofline(c, st):

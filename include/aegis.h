@@ -59,6 +59,9 @@ int aegis_sync(aegis_ctx* ctx);
 uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t ext_index); /* <60 main, >=60 special */
 /* count of kernels this context launched (for the bench's gpu_launches claim) */
 uint64_t aegis_launch_count(const aegis_ctx* ctx);
+/* NTT butterfly arithmetic: 0 = 64-bit integer Shoup, 1 = exact FP64 (default).
+ * impl < 0 only queries.  Returns the active implementation. */
+int aegis_ntt_impl(int impl);
 
 /* ---- bundles (CtBundle, he_ir.hpp:57-74) --------------------------------- */
 int aegis_bundle_alloc(aegis_ctx* ctx, uint32_t lanes, uint32_t comps, uint32_t level,
@@ -136,9 +139,25 @@ int aegis_graph_build_params(const aegis_params* params, const aegis_model* mode
 int aegis_graph_load(aegis_ctx* ctx, const char* path, aegis_graph** out); /* heops text */
 int aegis_graph_dump(const aegis_graph* g, const char* path);
 int aegis_graph_info(const aegis_graph* g, uint64_t* ops, uint64_t* bundles);
-/* Restrict execution to token groups [tg_lo, tg_hi) of `tg_total` (lane
- * ownership for multi-GPU token-coherent placement, placement.hpp:175-182). */
-int aegis_graph_set_shard(aegis_graph* g, uint32_t tg_lo, uint32_t tg_hi);
+/* Multi-GPU token-coherent placement (placement.hpp:175-182):
+ * this context executes only the lanes rank `rank` of `world` owns.  With
+ * world <= token groups each rank owns whole token groups (no collective);
+ * with world = m * groups the m ranks of a group split its positions and each
+ * PCMM is reduce-scattered once through the reducer hook.  world <= 1 clears. */
+int aegis_graph_set_shard(aegis_graph* g, uint32_t world, uint32_t rank);
+/* reduce-scatter hook: sum words_per_rank*m u64 words at device pointer `buf`
+ * over the m ranks of token group `group` (NCCL uint64 sum), leaving this
+ * rank's share at buf + part*words_per_rank; return 0 on success. */
+typedef int (*aegis_reduce_fn)(void* user, uint64_t* buf, uint64_t words_per_rank, uint32_t group);
+int aegis_graph_set_reducer(aegis_graph* g, aegis_reduce_fn fn, void* user);
+/* lane ownership of bundle `bundle` under the current shard (1 = owned) */
+int aegis_graph_owned_lanes(const aegis_graph* g, uint32_t bundle, uint8_t* mask, uint32_t cap);
+int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* tg_lo, uint32_t* tg_hi,
+                           uint32_t* ranks_per_group, uint32_t* part);
+/* hoisted ModUp across the rotations of one source (bit-exact; default on) */
+int aegis_graph_set_hoisting(aegis_graph* g, int enable);
+/* bytes copied host->device / device->host by the last aegis_graph_run_host */
+int aegis_graph_io_bytes(const aegis_graph* g, uint64_t* h2d, uint64_t* d2h);
 /* Execute ops [0, max_ops) (all if < 0).  Bundles are allocated at first write
  * and freed after their last use.  If hashes != NULL, hashes[b] receives the
  * content hash of bundle b when it dies (0 if never materialised). */

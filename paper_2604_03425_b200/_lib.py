@@ -41,6 +41,7 @@ SIGNATURES = [
     ("aegis_sync", ctypes.c_int, [vp]),
     ("aegis_prime", u64, [vp, u32]),
     ("aegis_launch_count", u64, [vp]),
+    ("aegis_ntt_impl", ctypes.c_int, [ctypes.c_int]),
     ("aegis_bundle_alloc", ctypes.c_int, [vp, u32, u32, u32, ctypes.POINTER(vp)]),
     ("aegis_bundle_free", ctypes.c_int, [vp, vp]),
     ("aegis_bundle_upload", ctypes.c_int, [vp, vp, u64p, u64]),
@@ -68,6 +69,11 @@ SIGNATURES = [
     ("aegis_graph_dump", ctypes.c_int, [vp, ctypes.c_char_p]),
     ("aegis_graph_info", ctypes.c_int, [vp, u64p, u64p]),
     ("aegis_graph_set_shard", ctypes.c_int, [vp, u32, u32]),
+    ("aegis_graph_set_reducer", ctypes.c_int, [vp, vp, vp]),
+    ("aegis_graph_owned_lanes", ctypes.c_int, [vp, u32, ctypes.POINTER(ctypes.c_uint8), u32]),
+    ("aegis_graph_shard_info", ctypes.c_int, [vp, u32p, u32p, u32p, u32p, u32p]),
+    ("aegis_graph_set_hoisting", ctypes.c_int, [vp, ctypes.c_int]),
+    ("aegis_graph_io_bytes", ctypes.c_int, [vp, u64p, u64p]),
     ("aegis_graph_run", ctypes.c_int, [vp, vp, i64, u64p, u64]),
     ("aegis_graph_io_words", ctypes.c_int, [vp, u64p, u64p]),
     ("aegis_graph_host_inputs", ctypes.c_int, [vp, vp, vp, u64]),
@@ -76,6 +82,9 @@ SIGNATURES = [
     ("aegis_graph_free", ctypes.c_int, [vp]),
     ("aegis_graph_peak_bytes", u64, [vp]),
 ]
+
+# int (*)(void* user, uint64_t* buf, uint64_t words_per_rank, uint32_t group)
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32)
 
 _lib = None
 

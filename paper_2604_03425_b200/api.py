@@ -253,10 +253,45 @@ class Graph:
         self.lib.aegis_graph_key_ids(self.h, _u64p(a), n.value, ctypes.byref(n))
         return a
 
-    def set_shard(self, lo, hi):
-        rc = self.lib.aegis_graph_set_shard(self.h, lo, hi)
+    def set_shard(self, world, rank):
+        """Token-coherent lane ownership for rank `rank` of `world`."""
+        rc = self.lib.aegis_graph_set_shard(self.h, world, rank)
         if rc:
-            raise ValueError("bad shard")
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+
+    def shard_info(self):
+        v = [ctypes.c_uint32() for _ in range(5)]
+        self.lib.aegis_graph_shard_info(self.h, *[ctypes.byref(x) for x in v])
+        return dict(zip(["tg_total", "tg_lo", "tg_hi", "ranks_per_group", "part"], [x.value for x in v]))
+
+    def owned_lanes(self, bundle, lanes):
+        m = (ctypes.c_uint8 * lanes)()
+        rc = self.lib.aegis_graph_owned_lanes(self.h, bundle, m, lanes)
+        if rc:
+            raise ValueError("bad bundle")
+        return np.frombuffer(m, dtype=np.uint8).astype(bool)
+
+    def set_reducer(self, fn):
+        """fn(buf_ptr:int, words_per_rank:int, group:int) -> None; reduce-scatter
+        (uint64 sum) of words_per_rank * m words at the device pointer."""
+        def cb(user, buf, words, group):
+            try:
+                fn(buf, words, group)
+                return 0
+            except Exception as e:  # never let an exception cross the C boundary
+                import sys
+                print(f"aegis reducer failed: {e!r}", file=sys.stderr)
+                return 1
+        self._reducer = L.REDUCE_FN(cb)  # keep alive
+        self.lib.aegis_graph_set_reducer(self.h, ctypes.cast(self._reducer, ctypes.c_void_p), None)
+
+    def set_hoisting(self, enable):
+        self.lib.aegis_graph_set_hoisting(self.h, 1 if enable else 0)
+
+    def io_bytes(self):
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        self.lib.aegis_graph_io_bytes(self.h, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
 
     def run(self, max_ops=-1, hashes=False):
         if self.ctx is None:

@@ -10,6 +10,7 @@
 #include <sstream>
 
 #include "context.h"
+#include "executor.h"
 #include "heplan_ir.h"
 
 using aegis::Bundle;
@@ -80,257 +81,39 @@ struct aegis_graph {
   hp::HeOpGraph g;
   std::string header;
   uint64_t peak = 0;
-  u32 shard_lo = 0, shard_hi = 0xffffffffu;
+  std::unique_ptr<aegis::ShardPlan> shard;
+  aegis::ReduceFn reduce = nullptr;
+  void* reduce_user = nullptr;
+  int hoist = 1;
+  uint64_t h2d = 0, d2h = 0;
 };
 
 namespace {
-
-struct Exec {
-  Context& c;
-  const hp::HeOpGraph& g;
-  std::vector<Bundle*> buf;
-  std::vector<u32> alloc_comps, cur_comps;
-  std::vector<char> zero_first;
-  std::vector<int64_t> last_use;
-  unsigned long long* d_hash = nullptr;
-
-  Exec(Context& ctx, const hp::HeOpGraph& graph) : c(ctx), g(graph) {
-    const size_t nb = g.bundles.size();
-    buf.assign(nb, nullptr);
-    alloc_comps.resize(nb);
-    cur_comps.assign(nb, 0);
-    zero_first.assign(nb, 0);
-    last_use.assign(nb, -1);
-    std::vector<char> seen(nb, 0);
-    for (size_t i = 0; i < nb; ++i) alloc_comps[i] = g.bundles[i].components;
-    for (size_t i = 0; i < g.ops.size(); ++i) {
-      const hp::HeOp& op = g.ops[i];
-      last_use[op.out.bundle] = (int64_t)i;
-      for (auto& s : op.ins) last_use[s.bundle] = (int64_t)i;
-      if (op.kind == hp::HeOpKind::kCMult) alloc_comps[op.out.bundle] = 3;
-      if (!seen[op.out.bundle] && op.kind != hp::HeOpKind::kEncode) {
-        seen[op.out.bundle] = 1;
-        zero_first[op.out.bundle] = op.accumulate ? 1 : 0;
-      }
-    }
-    find_hoist_groups();
-  }
-
-  // ---- hoisted ModUp across rotations of one source ----------
-  // A group is a run of Rot ops reading the same (bundle, lanes, level) with no
-  // write to that bundle in between (the 63 diagonals of a PCMM / CCMM).
-  struct Group {
-    u32 src, lane0, count, level;
-    int64_t last = -1;
-    u32 size = 0;
-    u64* ext = nullptr;
-    u32 hoisted_lanes = 0;
-    bool prepared = false;
-  };
-  std::vector<Group> groups;
-  std::vector<int> group_of;  // per op (-1 = none)
-
-  void find_hoist_groups() {
-    group_of.assign(g.ops.size(), -1);
-    std::map<u32, int> open;  // src bundle -> open group
-    for (size_t i = 0; i < g.ops.size(); ++i) {
-      const hp::HeOp& op = g.ops[i];
-      if (op.kind == hp::HeOpKind::kRot) {
-        const hp::LaneSlice& s = op.ins[0];
-        auto it = open.find(s.bundle);
-        if (it != open.end()) {
-          Group& gr = groups[it->second];
-          if (gr.lane0 != s.lane || gr.count != s.lane_count || gr.level != op.use_level) open.erase(it);
-        }
-        it = open.find(s.bundle);
-        if (it == open.end()) {
-          groups.push_back(Group{s.bundle, s.lane, s.lane_count, op.use_level});
-          it = open.emplace(s.bundle, (int)groups.size() - 1).first;
-        }
-        Group& gr = groups[it->second];
-        gr.last = (int64_t)i;
-        ++gr.size;
-        group_of[i] = it->second;
-      }
-      if (op.kind != hp::HeOpKind::kEncode) open.erase(op.out.bundle);  // the source is being overwritten
-    }
-  }
-
-  // memory the hoisted ModUp may use: leave room for the rotation outputs and
-  // the key-switch workspace
-  size_t hoist_budget(size_t out_bytes) {
-    size_t fr = 0, total = 0;
-    cudaMemGetInfo(&fr, &total);
-    const size_t reserved = c.live_bytes + c.total_key_bytes() + ((size_t)c.n * 2 * 16 * aegis::kNumExt);
-    const size_t cap = (size_t)(0.92 * (double)total);
-    const size_t margin = out_bytes + ((size_t)6 << 30);
-    return cap > reserved + margin ? cap - reserved - margin : 0;
-  }
-
-  void rot(const hp::HeOp& op, int64_t i, Bundle& in, Bundle& out, u32 lanes, u32 L) {
-    const int gi = group_of[i];
-    if (gi < 0 || groups[gi].size < 2 || op.ins[0].lane_count != lanes || hoist_disabled) {
-      c.op_rot(out, op.out.lane, in, lm(op.ins[0]), lanes, L, op.rot_offset);
-      return;
-    }
-    Group& gr = groups[gi];
-    const size_t per_lane = c.modup_words_per_lane(L);
-    if (!gr.prepared) {
-      gr.prepared = true;
-      const size_t budget = hoist_budget(out.bytes);
-      gr.hoisted_lanes = (u32)std::min<size_t>(lanes, budget / (per_lane * 8));
-      if (gr.hoisted_lanes > 0) {
-        gr.ext = c.alloc(per_lane * gr.hoisted_lanes);
-        c.modup(in.view().limb(op.ins[0].lane, 1, 0, c.n), (size_t)in.comps * in.level * c.n, gr.hoisted_lanes, L,
-                gr.ext);
-      }
-    }
-    const u32 H = gr.hoisted_lanes;
-    if (H > 0)
-      c.op_rot_cached(out, op.out.lane, in, LaneMap{op.ins[0].lane, H}, H, L, op.rot_offset, gr.ext);
-    if (H < lanes)
-      c.op_rot(out, op.out.lane + H, in, LaneMap{op.ins[0].lane + H, lanes - H}, lanes - H, L, op.rot_offset);
-    if (gr.last == i && gr.ext) {
-      c.release(gr.ext);
-      gr.ext = nullptr;
-    }
-  }
-  bool hoist_disabled = false;
-  int64_t cur_op = 0;
-
-  Bundle& get(u32 id) {
-    if (!buf[id]) {
-      const hp::CtBundle& cb = g.bundles[id];
-      buf[id] = c.new_bundle(cb.lanes, std::max<u32>(2, alloc_comps[id]), cb.level, zero_first[id] != 0);
-      cur_comps[id] = 2;
-    }
-    return *buf[id];
-  }
-  Bundle& input(const hp::LaneSlice& s) {
-    if (!buf[s.bundle]) throw Error(AEGIS_ELOGIC, "op reads bundle " + g.bundles[s.bundle].tag + " before it is written");
-    return *buf[s.bundle];
-  }
-  void retire(u32 id) {
-    if (!buf[id]) return;
-    if (id == final_bundle && host_out) {
-      const Bundle& b = *buf[id];
-      // first 2 comps of every lane: [lane][2][level][N]
-      AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(host_out, (size_t)2 * b.level * c.n * 8, b.ptr,
-                                         (size_t)b.comps * b.level * c.n * 8, (size_t)2 * b.level * c.n * 8,
-                                         b.lanes, cudaMemcpyDeviceToHost, c.stream));
-    }
-    if (d_hash) {
-      AEGIS_CHECK_CUDA(aegis::launch_hash(buf[id]->view(), buf[id]->lanes, cur_comps[id], g.bundles[id].level, c.n,
-                                          d_hash + id, c.stream));
-      c.count();
-    }
-    c.free_bundle(buf[id]);
-    buf[id] = nullptr;
-  }
-
-  const u64* host_in = nullptr;  // graph inputs from host memory (end-to-end path)
-  u64* host_out = nullptr;       // final bundle to host memory
-  u32 final_bundle = 0xffffffffu;
-
-  void run(int64_t max_ops) {
-    size_t off = 0;
-    for (u32 in : g.graph_inputs) {
-      Bundle& b = get(in);
-      if (host_in) {
-        const size_t words = (size_t)b.lanes * 2 * b.level * c.n;
-        AEGIS_CHECK_CUDA(cudaMemcpyAsync(b.ptr, host_in + off, words * 8, cudaMemcpyHostToDevice, c.stream));
-        off += words;
-      } else {
-        AEGIS_CHECK_CUDA(aegis::launch_fill_uniform(b.view(), b.lanes, 2, b.level, c.n, c.seed_input, 1, in,
-                                                    c.d_ident, c.d_pc, c.stream));
-        c.count();
-      }
-    }
-    if (host_out && !g.ops.empty()) final_bundle = g.ops.back().out.bundle;
-    const int64_t nops = max_ops < 0 ? (int64_t)g.ops.size() : std::min<int64_t>(max_ops, (int64_t)g.ops.size());
-    for (int64_t i = 0; i < nops; ++i) {
-      const hp::HeOp& op = g.ops[i];
-      cur_op = i;
-      step(op);
-      std::set<u32> touched{op.out.bundle};
-      for (auto& s : op.ins) touched.insert(s.bundle);
-      for (u32 b : touched)
-        if (last_use[b] == i && i + 1 < (int64_t)g.ops.size()) retire(b);
-    }
-    for (u32 b = 0; b < buf.size(); ++b) retire(b);
-    for (auto& gr : groups)
-      if (gr.ext) {
-        c.release(gr.ext);
-        gr.ext = nullptr;
-      }
-  }
-
-  static LaneMap lm(const hp::LaneSlice& s) { return LaneMap{s.lane, s.lane_count}; }
-
-  void step(const hp::HeOp& op) {
-    const u32 L = op.use_level;
-    const u32 lanes = op.out.lane_count;
-    switch (op.kind) {
-      case hp::HeOpKind::kEncode:
-        return;  // weights are generated inside the PMult kernel (kGenerate)
-      case hp::HeOpKind::kRot: {
-        Bundle& in = input(op.ins[0]);
-        Bundle& out = get(op.out.bundle);
-        rot(op, cur_op, in, out, lanes, L);
-        cur_comps[op.out.bundle] = 2;
-        return;
-      }
-      case hp::HeOpKind::kRelin: {
-        Bundle& b = get(op.out.bundle);
-        c.op_relin(b, op.out.lane, lanes, L);
-        cur_comps[op.out.bundle] = 2;
-        return;
-      }
-      case hp::HeOpKind::kRescale: {
-        Bundle& in = input(op.ins[0]);
-        Bundle& out = get(op.out.bundle);
-        c.op_rescale(out, op.out.lane, in, lm(op.ins[0]), lanes, L);
-        cur_comps[op.out.bundle] = 2;
-        return;
-      }
-      case hp::HeOpKind::kBoot: {
-        Bundle& in = input(op.ins[0]);
-        Bundle& out = get(op.out.bundle);
-        c.op_boot(out, op.out.lane, in, lm(op.ins[0]), lanes, L, g.bundles[op.out.bundle].level);
-        cur_comps[op.out.bundle] = 2;
-        return;
-      }
-      case hp::HeOpKind::kCMult: {
-        Bundle& a = input(op.ins[0]);
-        Bundle& b = input(op.ins[1]);
-        Bundle& out = get(op.out.bundle);
-        c.op_cmult(out, op.out.lane, lanes, a, lm(op.ins[0]), b, lm(op.ins[1]), L);
-        cur_comps[op.out.bundle] = 3;
-        return;
-      }
-      case hp::HeOpKind::kCAdd: {
-        Bundle& a = input(op.ins[0]);
-        Bundle* b = op.ins.size() > 1 ? &input(op.ins[1]) : nullptr;
-        Bundle& out = get(op.out.bundle);
-        c.op_cadd(out, op.out.lane, lanes, a, lm(op.ins[0]), b, b ? lm(op.ins[1]) : LaneMap{0, 1}, L, op.accumulate);
-        cur_comps[op.out.bundle] = 2;
-        return;
-      }
-      case hp::HeOpKind::kPMult: {
-        if (!op.accumulate || op.ins.size() != 2) throw Error(AEGIS_ELOGIC, "unsupported PMult form");
-        Bundle& x = input(op.ins[0]);
-        Bundle& acc = get(op.out.bundle);
-        c.op_pmult(acc, op.out.lane, lanes, g.bundles[op.out.bundle].chunk_period, x, op.ins[0].lane,
-                   op.ins[0].lane_count, op.ins[1].bundle, op.ins[1].lane_count, L);
-        cur_comps[op.out.bundle] = 2;
-        return;
-      }
-      case hp::HeOpKind::kPAdd:
-        throw Error(AEGIS_ELOGIC, "PAdd is not emitted by the reference lowering");
-    }
-  }
-};
-
+// "# heops v1 N=65536 ... T=2048 ..." -> value of `key=`
+uint64_t header_value(const std::string& h, const std::string& key) {
+  const size_t pos = h.find(" " + key + "=");
+  if (pos == std::string::npos) throw Error(AEGIS_EINVAL, "graph header lacks " + key);
+  return std::stoull(h.substr(pos + key.size() + 2));
+}
+uint32_t token_groups(const aegis_graph* g) {
+  const uint64_t n = header_value(g->header, "N"), T = header_value(g->header, "T"),
+                 stok = header_value(g->header, "stok");
+  const uint64_t per = n / 2 / stok;
+  return (uint32_t)((T + per - 1) / per);
+}
+void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
+  Context& c = *ctx->c;
+  opt.shard = g->shard.get();
+  opt.reduce = g->reduce;
+  opt.reduce_user = g->reduce_user;
+  opt.hoist = g->hoist != 0;
+  c.peak_bytes = c.live_bytes;
+  aegis::Executor ex(c, g->g, opt);
+  ex.run();
+  g->h2d = ex.h2d_bytes;
+  g->d2h = ex.d2h_bytes;
+  g->peak = c.peak_bytes;
+}
 }  // namespace
 
 // ===========================================================================
@@ -363,6 +146,10 @@ int aegis_sync(aegis_ctx* ctx) {
 }
 uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t e) { return e < aegis::kNumExt ? ctx->c->prime(e) : 0; }
 uint64_t aegis_launch_count(const aegis_ctx* ctx) { return ctx ? ctx->c->launches : 0; }
+int aegis_ntt_impl(int impl) {
+  if (impl == aegis::kNttInt || impl == aegis::kNttF64) aegis::g_ntt_impl = impl;
+  return aegis::g_ntt_impl;
+}
 
 int aegis_bundle_alloc(aegis_ctx* ctx, uint32_t lanes, uint32_t comps, uint32_t level, aegis_bundle** out) {
   return guard(ctx, [&] {
@@ -424,7 +211,7 @@ int aegis_bundle_hash(aegis_ctx* ctx, const aegis_bundle* b, uint32_t comps, uin
     Context& c = *ctx->c;
     u64* d = c.alloc(1);
     AEGIS_CHECK_CUDA(cudaMemsetAsync(d, 0, 8, c.stream));
-    AEGIS_CHECK_CUDA(aegis::launch_hash(bb.view(), bb.lanes, comps, level, c.n, (unsigned long long*)d, c.stream));
+    AEGIS_CHECK_CUDA(aegis::launch_hash(bb.view(), 0, bb.lanes, comps, level, c.n, (unsigned long long*)d, c.stream));
     c.count();
     AEGIS_CHECK_CUDA(cudaMemcpyAsync(out, d, 8, cudaMemcpyDeviceToHost, c.stream));
     AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.stream));
@@ -712,10 +499,53 @@ int aegis_graph_info(const aegis_graph* g, uint64_t* ops, uint64_t* bundles) {
   if (bundles) *bundles = g->g.bundles.size();
   return AEGIS_OK;
 }
-int aegis_graph_set_shard(aegis_graph* g, uint32_t lo, uint32_t hi) {
-  if (!g || lo >= hi) return AEGIS_EINVAL;
-  g->shard_lo = lo;
-  g->shard_hi = hi;
+int aegis_graph_set_shard(aegis_graph* g, uint32_t world, uint32_t rank) {
+  if (!g) return AEGIS_EINVAL;
+  return guard(nullptr, [&] {
+    if (world <= 1) {
+      g->shard.reset();
+      return;
+    }
+    g->shard.reset(new aegis::ShardPlan(aegis::make_shard_plan(g->g, token_groups(g), world, rank)));
+  });
+}
+int aegis_graph_set_reducer(aegis_graph* g, aegis_reduce_fn fn, void* user) {
+  if (!g) return AEGIS_EINVAL;
+  g->reduce = reinterpret_cast<aegis::ReduceFn>(fn);  // uint64_t* and u64* are the same 64-bit words
+  g->reduce_user = user;
+  return AEGIS_OK;
+}
+int aegis_graph_owned_lanes(const aegis_graph* g, uint32_t bundle, uint8_t* mask, uint32_t cap) {
+  if (!g || bundle >= g->g.bundles.size()) return AEGIS_EINVAL;
+  const uint32_t lanes = g->g.bundles[bundle].lanes;
+  for (uint32_t l = 0; l < lanes && l < cap; ++l) mask[l] = g->shard ? (g->shard->owns(bundle, l) ? 1 : 0) : 1;
+  return AEGIS_OK;
+}
+int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* tg_lo, uint32_t* tg_hi,
+                           uint32_t* ranks_per_group, uint32_t* part) {
+  if (!g) return AEGIS_EINVAL;
+  const aegis::ShardPlan* s = g->shard.get();
+  uint32_t tg = 1;
+  try {
+    tg = token_groups(g);
+  } catch (...) {
+  }
+  if (tg_total) *tg_total = tg;
+  if (tg_lo) *tg_lo = s ? s->tg_lo : 0;
+  if (tg_hi) *tg_hi = s ? s->tg_hi : tg;
+  if (ranks_per_group) *ranks_per_group = s ? s->m : 1;
+  if (part) *part = s ? s->part : 0;
+  return AEGIS_OK;
+}
+int aegis_graph_set_hoisting(aegis_graph* g, int enable) {
+  if (!g) return AEGIS_EINVAL;
+  g->hoist = enable;
+  return AEGIS_OK;
+}
+int aegis_graph_io_bytes(const aegis_graph* g, uint64_t* h2d, uint64_t* d2h) {
+  if (!g) return AEGIS_EINVAL;
+  if (h2d) *h2d = g->h2d;
+  if (d2h) *d2h = g->d2h;
   return AEGIS_OK;
 }
 int aegis_graph_key_ids(const aegis_graph* g, uint64_t* ids, uint32_t cap, uint32_t* n) {
@@ -738,15 +568,15 @@ int aegis_graph_run(aegis_ctx* ctx, aegis_graph* g, int64_t max_ops, uint64_t* h
     if (!g) throw Error(AEGIS_EINVAL, "null graph");
     Context& c = *ctx->c;
     const size_t nb = g->g.bundles.size();
-    Exec ex(c, g->g);
-    c.peak_bytes = c.live_bytes;
+    aegis::RunOptions opt;
+    opt.max_ops = max_ops;
     u64* dh = nullptr;
     if (hashes) {
       dh = c.alloc(nb);
       AEGIS_CHECK_CUDA(cudaMemsetAsync(dh, 0, nb * 8, c.stream));
-      ex.d_hash = (unsigned long long*)dh;
+      opt.d_hash = (unsigned long long*)dh;
     }
-    ex.run(max_ops);
+    run_graph(ctx, g, opt);
     if (hashes) {
       std::vector<u64> h(nb);
       AEGIS_CHECK_CUDA(cudaMemcpyAsync(h.data(), dh, nb * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -754,7 +584,6 @@ int aegis_graph_run(aegis_ctx* ctx, aegis_graph* g, int64_t max_ops, uint64_t* h
       for (size_t i = 0; i < nb && i < nhashes; ++i) hashes[i] = h[i];
       c.release(dh);
     }
-    g->peak = c.peak_bytes;
   });
 }
 int aegis_graph_io_words(const aegis_graph* g, uint64_t* in_words, uint64_t* out_words) {
@@ -802,13 +631,11 @@ int aegis_graph_run_host(aegis_ctx* ctx, aegis_graph* g, const uint64_t* in, uin
     aegis_graph_io_words(g, &wi, &wo);
     if (wi != in_words || wo != out_words) throw Error(AEGIS_EINVAL, "host buffer size mismatch");
     Context& c = *ctx->c;
-    Exec ex(c, g->g);
-    c.peak_bytes = c.live_bytes;
-    ex.host_in = reinterpret_cast<const u64*>(in);
-    ex.host_out = reinterpret_cast<u64*>(out);
-    ex.run(-1);
+    aegis::RunOptions opt;
+    opt.host_in = reinterpret_cast<const u64*>(in);
+    opt.host_out = reinterpret_cast<u64*>(out);
+    run_graph(ctx, g, opt);
     AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.stream));
-    g->peak = c.peak_bytes;
   });
 }
 int aegis_graph_free(aegis_graph* g) {

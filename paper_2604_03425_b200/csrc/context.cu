@@ -657,26 +657,35 @@ void Context::op_cadd(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, Lan
 }
 
 void Context::op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
-                       u32 x_lanes, u32 wbundle, u32 wlanes, u32 level) {
-  // token groups: in = tg*c_in, out = tg*c_out, w = c_in*c_out
-  u64 tg = 1;
-  while (tg * tg * wlanes < (u64)x_lanes * acc_lanes) ++tg;
-  if (tg * tg * wlanes != (u64)x_lanes * acc_lanes || x_lanes % tg || acc_lanes % tg)
-    throw Error(AEGIS_ELOGIC, "PMult lane shapes inconsistent");
-  const u32 c_in = (u32)(x_lanes / tg), c_out = (u32)(acc_lanes / tg);
-  if ((u64)c_in * c_out != wlanes) throw Error(AEGIS_ELOGIC, "PMult weight lanes inconsistent");
-  const u32 S = (chunk_period == 0 || chunk_period >= acc_lanes) ? 1 : acc_lanes / chunk_period;
-  if (c_out % S) throw Error(AEGIS_ELOGIC, "PMult sub-tensor split inconsistent");
-  const u32 c_sub = c_out / S;
+                       u32 x_lanes, u32 wbundle, u32 wlanes, u32 level, u32 t_lo, u32 t_hi, u32 ci_lo,
+                       u32 ci_hi) {
+  const PcmmShape sh = pcmm_shape(x_lanes, acc_lanes, wlanes, chunk_period);
+  t_hi = std::min(t_hi, sh.tg);
+  ci_hi = std::min(ci_hi, sh.c_in);
+  if (t_lo >= t_hi || ci_lo >= ci_hi) return;
   u64* rk = alloc((size_t)wlanes * level);
   AEGIS_CHECK_CUDA(launch_weight_rowkeys(rk, wlanes, level, seed_weight, wbundle, stream));
   count();
-  for (u32 s = 0; s < S; ++s) {
-    // sub-tensor s occupies acc lanes [s*chunk_period, (s+1)*chunk_period), token-major inside
-    const u32 lane0 = acc_lane + s * (S == 1 ? 0 : chunk_period);
-    AEGIS_CHECK_CUDA(launch_pmult_acc(acc.view(), lane0, x.view(), x_lane, (u32)tg, c_in, c_sub, s * c_sub, c_out,
-                                      level, n, rk, d_pc, stream));
-    count((tg + 3) / 4);
+  for (u32 s = 0; s < sh.S; ++s) {
+    // sub-tensor s occupies acc lanes [s*chunk, (s+1)*chunk), token-major inside
+    PmultArgs a;
+    a.acc = acc.view();
+    a.acc_lane0 = acc_lane + pcmm_lane(sh, t_lo, s * sh.c_sub);
+    a.acc_tstride = sh.S == 1 ? sh.c_out : sh.c_sub;
+    a.x = x.view();
+    a.x_lane0 = x_lane + t_lo * sh.c_in + ci_lo;
+    a.x_tstride = sh.c_in;
+    a.tg = t_hi - t_lo;
+    a.c_in = ci_hi - ci_lo;
+    a.c_out = sh.c_sub;
+    a.ci_off = ci_lo;
+    a.o_off = s * sh.c_sub;
+    a.w_cout = sh.c_out;
+    a.limbs = level;
+    a.n = n;
+    a.rowkeys = rk;
+    AEGIS_CHECK_CUDA(launch_pmult_acc(a, d_pc, stream));
+    count((a.tg + 3) / 4);
   }
   release(rk);
 }

@@ -10,6 +10,7 @@
 #include "../../include/aegis.h"
 #include "kernels.h"
 #include "ntt.h"
+#include "shard.h"
 
 namespace aegis {
 
@@ -118,8 +119,11 @@ class Context {
                 LaneMap mb, u32 level);
   void op_cadd(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, LaneMap ma, const Bundle* b,
                LaneMap mb, u32 level, bool acc);
+  // token groups [t_lo, t_hi) and input positions [ci_lo, ci_hi) of the PCMM
+  // step (defaults: everything); a position subset yields partial sums.
   void op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
-                u32 x_lanes, u32 wbundle, u32 wlanes, u32 level);
+                u32 x_lanes, u32 wbundle, u32 wlanes, u32 level, u32 t_lo = 0, u32 t_hi = ~0u, u32 ci_lo = 0,
+                u32 ci_hi = ~0u);
 
   void count(u64 k = 1) { launches += k; }
   std::string last_error;

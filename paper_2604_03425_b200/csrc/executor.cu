@@ -1,0 +1,383 @@
+// executor.cu -- HE-op graph executor (see executor.h).
+//
+// Replays the reference's op list verbatim (he_ir.hpp:683 output), op by op
+// on the context stream.  Memory: a bundle is allocated when first written
+// (zeroed only if its first writer accumulates) and freed after its last use.
+// Rotations reading the same source between writes form a group whose ModUp is
+// computed once (bit-exact hoisting).  Under a ShardPlan every
+// op touches only the lanes this rank owns; PCMM with several ranks per token
+// group accumulates partial sums that are reduce-scattered before the rescale.
+#include <algorithm>
+#include <map>
+#include <set>
+
+#include "executor.h"
+
+namespace aegis {
+
+namespace hp = heplan;
+
+Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& opt)
+    : c(ctx), g(graph), o(opt) {
+  const size_t nb = g.bundles.size();
+  buf.assign(nb, nullptr);
+  alloc_comps.resize(nb);
+  cur_comps.assign(nb, 0);
+  zero_first.assign(nb, 0);
+  partial.assign(nb, 0);
+  last_use.assign(nb, -1);
+  std::vector<char> seen(nb, 0);
+  for (size_t i = 0; i < nb; ++i) alloc_comps[i] = g.bundles[i].components;
+  for (size_t i = 0; i < g.ops.size(); ++i) {
+    const hp::HeOp& op = g.ops[i];
+    last_use[op.out.bundle] = (int64_t)i;
+    for (auto& s : op.ins) last_use[s.bundle] = (int64_t)i;
+    if (op.kind == hp::HeOpKind::kCMult) alloc_comps[op.out.bundle] = 3;
+    if (!seen[op.out.bundle] && op.kind != hp::HeOpKind::kEncode) {
+      seen[op.out.bundle] = 1;
+      zero_first[op.out.bundle] = op.accumulate ? 1 : 0;
+    }
+  }
+  if (o.shard && !o.shard->active()) o.shard = nullptr;
+  find_hoist_groups();
+}
+
+Executor::~Executor() {
+  for (auto& gr : groups)
+    if (gr.ext) c.release(gr.ext);
+  for (auto* b : buf)
+    if (b) c.free_bundle(b);
+}
+
+Bundle& Executor::get(u32 id) {
+  if (!buf[id]) {
+    const hp::CtBundle& cb = g.bundles[id];
+    buf[id] = c.new_bundle(cb.lanes, std::max<u32>(2, alloc_comps[id]), cb.level, zero_first[id] != 0);
+    cur_comps[id] = 2;
+  }
+  return *buf[id];
+}
+
+Bundle& Executor::input(const hp::LaneSlice& s) {
+  if (!buf[s.bundle]) throw Error(AEGIS_ELOGIC, "op reads bundle " + g.bundles[s.bundle].tag + " before it is written");
+  if (partial[s.bundle]) reduce_partial(s.bundle);
+  return *buf[s.bundle];
+}
+
+void Executor::retire(u32 id) {
+  if (!buf[id]) return;
+  if (partial[id]) reduce_partial(id);
+  const Bundle& b = *buf[id];
+  const hp::CtBundle& cb = g.bundles[id];
+  std::vector<std::pair<u32, u32>> runs =
+      o.shard ? o.shard->runs(id, 0, cb.lanes) : std::vector<std::pair<u32, u32>>{{0, cb.lanes}};
+  if (id == final_bundle && o.host_out) {
+    // first 2 comps of every owned lane: host layout [lane][2][level][N]
+    const size_t lane_words = (size_t)2 * cb.level * c.n;
+    for (auto [s, e] : runs) {
+      AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(o.host_out + (size_t)s * lane_words, lane_words * 8,
+                                         b.view().limb(s, 0, 0, c.n), (size_t)b.comps * b.level * c.n * 8,
+                                         lane_words * 8, e - s, cudaMemcpyDeviceToHost, c.stream));
+      d2h_bytes += (size_t)(e - s) * lane_words * 8;
+    }
+  }
+  if (o.d_hash) {
+    for (auto [s, e] : runs) {
+      AEGIS_CHECK_CUDA(launch_hash(b.view(), s, e - s, cur_comps[id], cb.level, c.n, o.d_hash + id, c.stream));
+      c.count();
+    }
+  }
+  c.free_bundle(buf[id]);
+  buf[id] = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+void Executor::find_hoist_groups() {
+  group_of.assign(g.ops.size(), -1);
+  std::map<u32, int> open;  // src bundle -> open group
+  for (size_t i = 0; i < g.ops.size(); ++i) {
+    const hp::HeOp& op = g.ops[i];
+    if (op.kind == hp::HeOpKind::kRot) {
+      const hp::LaneSlice& s = op.ins[0];
+      auto it = open.find(s.bundle);
+      if (it != open.end()) {
+        const Group& gr = groups[it->second];
+        if (gr.lane0 != s.lane || gr.count != s.lane_count || gr.level != op.use_level) open.erase(it);
+      }
+      it = open.find(s.bundle);
+      if (it == open.end()) {
+        Group ng;
+        ng.src = s.bundle;
+        ng.lane0 = s.lane;
+        ng.count = s.lane_count;
+        ng.level = op.use_level;
+        groups.push_back(ng);
+        it = open.emplace(s.bundle, (int)groups.size() - 1).first;
+      }
+      Group& gr = groups[it->second];
+      gr.last = (int64_t)i;
+      ++gr.size;
+      group_of[i] = it->second;
+    }
+    if (op.kind != hp::HeOpKind::kEncode) open.erase(op.out.bundle);  // the source is overwritten
+  }
+}
+
+// Memory the hoisted ModUp may use: leave room for the rotation outputs, the
+// keys and the key-switch workspace.
+size_t Executor::hoist_budget(size_t out_bytes) {
+  size_t fr = 0, total = 0;
+  cudaMemGetInfo(&fr, &total);
+  const size_t reserved = c.live_bytes + c.total_key_bytes() + ((size_t)c.n * 4 * 16 * kNumExt);
+  const size_t cap = (size_t)(0.92 * (double)total);
+  const size_t margin = out_bytes + ((size_t)6 << 30);
+  return cap > reserved + margin ? cap - reserved - margin : 0;
+}
+
+void Executor::rot_run(const hp::HeOp& op, int64_t i, u32 pos, u32 len) {
+  Bundle& in = input(op.ins[0]);
+  Bundle& out = get(op.out.bundle);
+  const u32 L = op.use_level;
+  const int gi = group_of[i];
+  const u32 src0 = op.ins[0].lane + pos;  // Rot reads lane l of the source for output lane l
+  if (!o.hoist || gi < 0 || groups[gi].size < 2 || op.ins[0].lane_count != op.out.lane_count) {
+    c.op_rot(out, op.out.lane + pos, in, LaneMap{src0, len}, len, L, op.rot_offset);
+    return;
+  }
+  Group& gr = groups[gi];
+  const size_t per_lane = c.modup_words_per_lane(L);
+  if (!gr.prepared) {
+    gr.prepared = true;
+    gr.runs = o.shard ? o.shard->runs(gr.src, gr.lane0, gr.count)
+                      : std::vector<std::pair<u32, u32>>{{gr.lane0, gr.lane0 + gr.count}};
+    u32 total = 0;
+    for (auto [s, e] : gr.runs) {
+      gr.run_off.push_back(total);
+      total += e - s;
+    }
+    gr.hoisted = (u32)std::min<size_t>(total, hoist_budget(out.bytes) / (per_lane * 8));
+    if (gr.hoisted > 0) {
+      gr.ext = c.alloc(per_lane * gr.hoisted);
+      const size_t in_ls = (size_t)in.comps * in.level * c.n;
+      for (size_t r = 0; r < gr.runs.size(); ++r) {
+        const u32 off = gr.run_off[r];
+        if (off >= gr.hoisted) break;
+        const u32 cnt = std::min(gr.runs[r].second - gr.runs[r].first, gr.hoisted - off);
+        c.modup(in.view().limb(gr.runs[r].first, 1, 0, c.n), in_ls, cnt, L, gr.ext + (size_t)off * per_lane);
+      }
+    }
+  }
+  // locate [src0, src0+len) in the compact (run-ordered) ext buffer
+  u32 done = 0;
+  while (done < len) {
+    const u32 lane = src0 + done;
+    size_t r = 0;
+    while (r < gr.runs.size() && !(lane >= gr.runs[r].first && lane < gr.runs[r].second)) ++r;
+    if (r == gr.runs.size()) throw Error(AEGIS_ELOGIC, "rotation of a lane this rank does not own");
+    const u32 idx = gr.run_off[r] + (lane - gr.runs[r].first);
+    u32 cnt = std::min(len - done, gr.runs[r].second - lane);
+    if (idx < gr.hoisted) {
+      cnt = std::min(cnt, gr.hoisted - idx);
+      c.op_rot_cached(out, op.out.lane + pos + done, in, LaneMap{lane, cnt}, cnt, L, op.rot_offset,
+                      gr.ext + (size_t)idx * per_lane);
+    } else {
+      c.op_rot(out, op.out.lane + pos + done, in, LaneMap{lane, cnt}, cnt, L, op.rot_offset);
+    }
+    done += cnt;
+  }
+}
+
+// ---------------------------------------------------------------------------
+std::vector<std::pair<u32, u32>> Executor::out_runs(const hp::HeOp& op) const {
+  const u32 n = op.out.lane_count;
+  std::vector<std::pair<u32, u32>> r;
+  if (!o.shard) {
+    r.emplace_back(0, n);
+    return r;
+  }
+  for (auto [s, e] : o.shard->runs(op.out.bundle, op.out.lane, n)) r.emplace_back(s - op.out.lane, e - op.out.lane);
+  return r;
+}
+
+// first position >= pos where a wrapped operand (count != n) wraps around
+u32 Executor::wrap_end(const hp::HeOp& op, u32 pos, u32 end) const {
+  const u32 n = op.out.lane_count;
+  for (const hp::LaneSlice& s : op.ins)
+    if (s.lane_count != n && s.lane_count) end = std::min(end, (pos / s.lane_count + 1) * s.lane_count);
+  return end;
+}
+
+LaneMap Executor::sub_map(const hp::LaneSlice& s, u32 n, u32 pos, u32 len) {
+  return s.lane_count == n ? LaneMap{s.lane + pos, len} : LaneMap{s.lane + pos % s.lane_count, len};
+}
+
+void Executor::pmult(const hp::HeOp& op) {
+  if (!op.accumulate || op.ins.size() != 2) throw Error(AEGIS_ELOGIC, "unsupported PMult form");
+  Bundle& x = input(op.ins[0]);
+  Bundle& acc = get(op.out.bundle);
+  const u32 chunk = g.bundles[op.out.bundle].chunk_period;
+  const u32 L = op.use_level;
+  if (!o.shard) {
+    c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
+               op.ins[1].lane_count, L);
+    return;
+  }
+  const ShardPlan& P = *o.shard;
+  if (P.m == 1) {
+    c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
+               op.ins[1].lane_count, L, P.tg_lo, P.tg_hi);
+    return;
+  }
+  // input-stationary: this rank's input positions into every output of its group
+  const PcmmShape sh = pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count, chunk);
+  const u32 t = P.tg_lo;
+  u32 ci_lo = sh.c_in, ci_hi = 0;
+  for (u32 ci = 0; ci < sh.c_in; ++ci)
+    if (P.owns(op.ins[0].bundle, op.ins[0].lane + t * sh.c_in + ci)) {
+      ci_lo = std::min(ci_lo, ci);
+      ci_hi = std::max(ci_hi, ci + 1);
+    }
+  if (ci_lo < ci_hi)
+    c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
+               op.ins[1].lane_count, L, t, t + 1, ci_lo, ci_hi);
+  partial[op.out.bundle] = 1;
+}
+
+// Sum the partial accumulators of this rank's token group over its m ranks
+// (one reduce-scatter per sub-tensor) and canonicalise the owned share.
+void Executor::reduce_partial(u32 b) {
+  partial[b] = 0;
+  if (!o.shard || o.shard->m == 1) return;
+  if (!o.reduce) throw Error(AEGIS_ELOGIC, "sharded PCMM needs a reduce-scatter hook (aegis_graph_set_reducer)");
+  const ShardPlan& P = *o.shard;
+  Bundle& acc = *buf[b];
+  // find the PCMM shape from the last PMult writing this bundle
+  const hp::HeOp* pm = nullptr;
+  for (const hp::HeOp& op : g.ops)
+    if (op.kind == hp::HeOpKind::kPMult && op.out.bundle == b) pm = &op;
+  if (!pm) throw Error(AEGIS_ELOGIC, "partial bundle without a PCMM writer");
+  const PcmmShape sh = pcmm_shape(pm->ins[0].lane_count, pm->out.lane_count, pm->ins[1].lane_count,
+                                  g.bundles[b].chunk_period);
+  if (sh.c_sub % P.m) throw Error(AEGIS_EINVAL, "PCMM outputs do not split evenly over the ranks of a token group");
+  const u32 t = P.tg_lo, share = sh.c_sub / P.m;
+  const uint64_t words_per_lane = (uint64_t)acc.comps * acc.level * c.n;
+  AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.stream));
+  for (u32 s = 0; s < sh.S; ++s) {
+    const u32 lane0 = pm->out.lane + pcmm_lane(sh, t, s * sh.c_sub);
+    u64* base = acc.view().limb(lane0, 0, 0, c.n);
+    if (o.reduce(o.reduce_user, base, words_per_lane * share, t) != 0)
+      throw Error(AEGIS_ENCCL, "reduce-scatter hook failed");
+    AEGIS_CHECK_CUDA(launch_reduce_lanes(acc.view(), lane0 + P.part * share, share, acc.comps, acc.level, c.n, c.d_pc,
+                                         c.stream));
+    c.count();
+  }
+}
+
+void Executor::step(const hp::HeOp& op, int64_t i) {
+  using K = hp::HeOpKind;
+  const u32 L = op.use_level;
+  if (op.kind == K::kEncode) return;  // weights are generated inside the PMult kernel (kGenerate)
+  if (op.kind == K::kPAdd) throw Error(AEGIS_ELOGIC, "PAdd is not emitted by the reference lowering");
+  if (op.kind == K::kPMult) {
+    pmult(op);
+    cur_comps[op.out.bundle] = 2;
+    return;
+  }
+  if (partial[op.out.bundle]) reduce_partial(op.out.bundle);
+  const u32 n = op.out.lane_count;
+  for (auto [rs, re] : out_runs(op)) {
+    for (u32 pos = rs; pos < re;) {
+      const u32 end = wrap_end(op, pos, re);
+      const u32 len = end - pos;
+      switch (op.kind) {
+        case K::kRot:
+          rot_run(op, i, pos, len);
+          break;
+        case K::kRelin:
+          c.op_relin(get(op.out.bundle), op.out.lane + pos, len, L);
+          break;
+        case K::kRescale: {
+          Bundle& in = input(op.ins[0]);
+          c.op_rescale(get(op.out.bundle), op.out.lane + pos, in, sub_map(op.ins[0], n, pos, len), len, L);
+          break;
+        }
+        case K::kBoot: {
+          Bundle& in = input(op.ins[0]);
+          c.op_boot(get(op.out.bundle), op.out.lane + pos, in, sub_map(op.ins[0], n, pos, len), len, L,
+                    g.bundles[op.out.bundle].level);
+          break;
+        }
+        case K::kCMult: {
+          Bundle& a = input(op.ins[0]);
+          Bundle& b = input(op.ins[1]);
+          c.op_cmult(get(op.out.bundle), op.out.lane + pos, len, a, sub_map(op.ins[0], n, pos, len), b,
+                     sub_map(op.ins[1], n, pos, len), L);
+          break;
+        }
+        case K::kCAdd: {
+          Bundle& a = input(op.ins[0]);
+          Bundle* b = op.ins.size() > 1 ? &input(op.ins[1]) : nullptr;
+          c.op_cadd(get(op.out.bundle), op.out.lane + pos, len, a, sub_map(op.ins[0], n, pos, len), b,
+                    b ? sub_map(op.ins[1], n, pos, len) : LaneMap{0, 1}, L, op.accumulate);
+          break;
+        }
+        default:
+          throw Error(AEGIS_ELOGIC, "unknown op kind");
+      }
+      pos = end;
+    }
+  }
+  // a rank that owns no output lane of this op still materialises the bundle
+  // so later readers find it (its lanes are never touched)
+  get(op.out.bundle);
+  cur_comps[op.out.bundle] = op.kind == K::kCMult ? 3 : 2;
+  if (op.kind == K::kRot && group_of[i] >= 0) {
+    Group& gr = groups[group_of[i]];
+    if (gr.last == i && gr.ext) {
+      c.release(gr.ext);
+      gr.ext = nullptr;
+    }
+  }
+}
+
+void Executor::run() {
+  // graph inputs: synthetic (PRNG tag 1) or copied from host memory
+  size_t off = 0;
+  for (u32 in : g.graph_inputs) {
+    Bundle& b = get(in);
+    const size_t lane_words = (size_t)2 * b.level * c.n;
+    std::vector<std::pair<u32, u32>> runs =
+        o.shard ? o.shard->runs(in, 0, b.lanes) : std::vector<std::pair<u32, u32>>{{0, b.lanes}};
+    if (o.host_in) {
+      for (auto [s, e] : runs) {
+        AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(b.view().limb(s, 0, 0, c.n), (size_t)b.comps * b.level * c.n * 8,
+                                           o.host_in + off + (size_t)s * lane_words, lane_words * 8, lane_words * 8,
+                                           e - s, cudaMemcpyHostToDevice, c.stream));
+        h2d_bytes += (size_t)(e - s) * lane_words * 8;
+      }
+      off += (size_t)b.lanes * lane_words;
+    } else {
+      AEGIS_CHECK_CUDA(launch_fill_uniform(b.view(), b.lanes, 2, b.level, c.n, c.seed_input, 1, in, c.d_ident, c.d_pc,
+                                           c.stream));
+      c.count();
+    }
+  }
+  if (o.host_out && !g.ops.empty()) final_bundle = g.ops.back().out.bundle;
+  const int64_t nops = o.max_ops < 0 ? (int64_t)g.ops.size() : std::min<int64_t>(o.max_ops, (int64_t)g.ops.size());
+  for (int64_t i = 0; i < nops; ++i) {
+    const hp::HeOp& op = g.ops[i];
+    step(op, i);
+    std::set<u32> touched{op.out.bundle};
+    for (auto& s : op.ins) touched.insert(s.bundle);
+    for (u32 b : touched)
+      if (last_use[b] == i && i + 1 < (int64_t)g.ops.size()) retire(b);
+  }
+  for (u32 b = 0; b < buf.size(); ++b) retire(b);
+  for (auto& gr : groups)
+    if (gr.ext) {
+      c.release(gr.ext);
+      gr.ext = nullptr;
+    }
+}
+
+}  // namespace aegis

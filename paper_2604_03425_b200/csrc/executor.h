@@ -1,0 +1,75 @@
+// executor.h -- runs a bundled HE-op graph (he_ir.hpp:57-120) on one GPU:
+// SPEC.md:407-415 exec_sequential, plus exec_plan-style lane sharding for
+// multi-GPU token-coherent placement (shard.h).
+#pragma once
+
+#include <vector>
+
+#include "context.h"
+#include "heplan_ir.h"
+#include "shard.h"
+
+namespace aegis {
+
+// Reduce-scatter hook for sharded PCMM (world > token groups): sum the
+// `words_per_rank * m` words at `buf` across the m ranks of token group `group`
+// and leave this rank's share (ncclUint64 sum semantics) at `buf + part * words_per_rank`.
+// Called with the compute stream idle; must return after the data is in place.
+typedef int (*ReduceFn)(void* user, u64* buf, uint64_t words_per_rank, uint32_t group);
+
+struct RunOptions {
+  int64_t max_ops = -1;
+  unsigned long long* d_hash = nullptr;  // per-bundle hash slots (owned lanes only)
+  const u64* host_in = nullptr;          // graph inputs from host memory
+  u64* host_out = nullptr;               // final bundle to host memory
+  const ShardPlan* shard = nullptr;
+  ReduceFn reduce = nullptr;
+  void* reduce_user = nullptr;
+  bool hoist = true;
+};
+
+class Executor {
+ public:
+  Executor(Context& c, const heplan::HeOpGraph& g, const RunOptions& opt);
+  ~Executor();
+  void run();
+  size_t h2d_bytes = 0, d2h_bytes = 0;
+
+ private:
+  struct Group {  // Rot ops sharing one source (hoisted ModUp)
+    u32 src, lane0, count, level;
+    int64_t last = -1;
+    u32 size = 0;
+    u64* ext = nullptr;
+    bool prepared = false;
+    std::vector<std::pair<u32, u32>> runs;  // owned source runs (absolute lanes)
+    std::vector<u32> run_off;               // compact ext offset (lanes) of each run
+    u32 hoisted = 0;                        // lanes (in run order) whose ModUp is cached
+  };
+
+  Bundle& get(u32 id);
+  Bundle& input(const heplan::LaneSlice& s);
+  void retire(u32 id);
+  void find_hoist_groups();
+  size_t hoist_budget(size_t out_bytes);
+  void step(const heplan::HeOp& op, int64_t i);
+  void pmult(const heplan::HeOp& op);
+  void rot_run(const heplan::HeOp& op, int64_t i, u32 r0, u32 len);
+  void reduce_partial(u32 bundle);
+  std::vector<std::pair<u32, u32>> out_runs(const heplan::HeOp& op) const;
+  static LaneMap sub_map(const heplan::LaneSlice& s, u32 n, u32 pos, u32 len);
+  u32 wrap_end(const heplan::HeOp& op, u32 pos, u32 end) const;
+
+  Context& c;
+  const heplan::HeOpGraph& g;
+  RunOptions o;
+  std::vector<Bundle*> buf;
+  std::vector<u32> alloc_comps, cur_comps;
+  std::vector<char> zero_first, partial;
+  std::vector<int64_t> last_use;
+  std::vector<Group> groups;
+  std::vector<int> group_of;
+  u32 final_bundle = 0xffffffffu;
+};
+
+}  // namespace aegis

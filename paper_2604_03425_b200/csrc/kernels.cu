@@ -118,11 +118,11 @@ __global__ void copy_kernel(View dst, u32 dst_lane0, View src, LaneMap sm, u32 n
   for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads) d[t] = s[t];
 }
 
-__global__ void hash_kernel(View v, u32 comps, u32 limbs, u32 n, unsigned long long* out, u32 cpr) {
+__global__ void hash_kernel(View v, u32 lane0, u32 comps, u32 limbs, u32 n, unsigned long long* out, u32 cpr) {
   const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
-  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, lane = rest / comps;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, lane = lane0 + rest / comps;
   const u64* s = v.limb(lane, comp, lb, n);
-  const u64 base = (u64)row * n;  // dense position of (lane, comp, limb, 0)
+  const u64 base = ((u64)lane * comps * limbs + (u64)comp * limbs + lb) * n;  // dense position
   u64 h = 0;
   for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
     h += mix64(s[t] + (base + t) * kGold);
@@ -184,9 +184,10 @@ __device__ __noinline__ u64 tie_resolve(const ConvPlanDev* __restrict__ pl, cons
 template <int K>
 __global__ void __launch_bounds__(256) basis_convert_kernel(const ConvPlanDev* __restrict__ pl,
                                                             const u64* __restrict__ hat_tab, const ConvIO io,
-                                                            u32 n, u32 kdyn, u32 m) {
+                                                            u32 lanes, u32 n, u32 kdyn, u32 m) {
   const u32 k = K > 0 ? (u32)K : kdyn;
   const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= lanes * n) return;
   const u32 lane = gid / n, x = gid - lane * n;
   const u64* src = io.src + (size_t)lane * io.src_lane_stride + x;
   u64* dst = io.dst + (size_t)lane * io.dst_lane_stride + x;
@@ -235,8 +236,11 @@ __global__ void __launch_bounds__(256) basis_convert_kernel(const ConvPlanDev* _
 // ---------------------------------------------------------------------------
 __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeConst* __restrict__ pc,
                               u32 cpr) {
-  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
-  const u32 slot = row % io.nslots, lane = row / io.nslots;
+  // lanes vary fastest across the grid: CTAs running together share the key
+  // limbs of one slot, so a batch streams each key limb from HBM once (L2 hits
+  // for the other lanes) instead of once per lane.
+  const u32 lane = blockIdx.x % lanes, rest = blockIdx.x / lanes;
+  const u32 chunk = rest % cpr, slot = rest / cpr;
   const u32 e = io.slot_ext[slot];
   const PrimeConst P = pc[e];
   const u32 ks = io.slot_key[slot];
@@ -275,7 +279,7 @@ __global__ void finish_kernel(const FinishIO io, u32 n, const PrimeConst* __rest
     // optional eval-domain automorphism of the result: read position pi(t)
     // (maps aligned 32-blocks onto aligned 32-blocks, so the gather coalesces)
     u32 s = t;
-    if (k != 1) s = __brev(((((__brev(t) >> sh) * 2 + 1) * k & mask) - 1) >> 1) >> sh;
+    if (k > 1) s = __brev(((((__brev(t) >> sh) * 2 + 1) * k & mask) - 1) >> 1) >> sh;
     u64 r = shoup(sub_mod(x[s], y[s], p), f, fp, p);
     if (ad) r = add_mod(r, ad[s], p);
     o[t] = r;
@@ -292,12 +296,9 @@ constexpr u32 kPmGroups = 8;   // o-groups per CTA (256 threads)
 // weight lane is ci*w_cout + o_off + o' (o_off/w_cout select one sub-tensor
 // of a chunked accumulator, CtBundle::chunk_period, he_ir.hpp:338).
 template <int TG>
-__global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, View X, u32 x_lane0,
-                                                    u32 c_in, u32 c_out, u32 o_off, u32 w_cout,
-                                                    u32 limbs, u32 n,
-                                                    const u64* __restrict__ rowkeys,
-                                                    const PrimeConst* __restrict__ pc) {
+__global__ void __launch_bounds__(256) pmult_kernel(const PmultArgs a, const PrimeConst* __restrict__ pc) {
   extern __shared__ Split xs[];  // [TG * c_in][2][kPmTx], pre-split into 24-bit limbs
+  const u32 n = a.n, c_in = a.c_in, c_out = a.c_out, limbs = a.limbs;
   const u32 tiles = n / kPmTx;
   const u32 lb = blockIdx.x / tiles;
   const u32 x0 = (blockIdx.x - lb * tiles) * kPmTx;
@@ -305,16 +306,18 @@ __global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, Vie
   const u32 nx = TG * c_in;
   for (u32 e = threadIdx.x; e < nx * 2 * kPmTx; e += blockDim.x) {
     const u32 xx = e % kPmTx, r = e / kPmTx, comp = r & 1, ln = r >> 1;
-    xs[e] = split24(X.limb(x_lane0 + ln, comp, lb, n)[x0 + xx]);
+    const u32 t = ln / c_in, ci = ln - t * c_in;
+    xs[e] = split24(a.x.limb(a.x_lane0 + t * a.x_tstride + ci, comp, lb, n)[x0 + xx]);
   }
   __syncthreads();
   const u32 xx = threadIdx.x % kPmTx;
   const u32 og = threadIdx.x / kPmTx;
   const u64 xi = x0 + xx;
+  const u64* __restrict__ rowkeys = a.rowkeys;
   for (u32 o = og; o < c_out; o += kPmGroups) {
     Acc3 s[TG][2];
     for (u32 ci = 0; ci < c_in; ++ci) {
-      const u64 rk = rowkeys[(size_t)(ci * w_cout + o_off + o) * limbs + lb];
+      const u64 rk = rowkeys[(size_t)((a.ci_off + ci) * a.w_cout + a.o_off + o) * limbs + lb];
       const Split w = split24(uniform_at(rk, xi, P.p, P.shift));
 #pragma unroll
       for (int t = 0; t < TG; ++t) {
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(256) pmult_kernel(View acc, u32 acc_lane0, Vie
     for (int t = 0; t < TG; ++t)
 #pragma unroll
       for (int cp = 0; cp < 2; ++cp) {
-        u64* d = acc.limb(acc_lane0 + t * c_out + o, cp, lb, n) + xi;
+        u64* d = a.acc.limb(a.acc_lane0 + t * a.acc_tstride + o, cp, lb, n) + xi;
         s[t][cp].c0 += *d;
         *d = acc3_reduce(s[t][cp], P.p, P.mu104);
       }
@@ -403,12 +406,32 @@ cudaError_t launch_copy(View dst, u32 dst_lane0, View src, LaneMap sm, u32 nlane
   return cudaGetLastError();
 }
 
-cudaError_t launch_hash(View v, u32 lanes, u32 comps, u32 limbs, u32 n, unsigned long long* out,
+cudaError_t launch_hash(View v, u32 lane0, u32 lanes, u32 comps, u32 limbs, u32 n, unsigned long long* out,
                         cudaStream_t st) {
   const u32 cpr = chunks_of(n);
   const size_t g = (size_t)lanes * comps * limbs * cpr;
   if (!g) return cudaSuccess;
-  hash_kernel<<<(unsigned)g, kThreads, 0, st>>>(v, comps, limbs, n, out, cpr);
+  hash_kernel<<<(unsigned)g, kThreads, 0, st>>>(v, lane0, comps, limbs, n, out, cpr);
+  return cudaGetLastError();
+}
+
+// values < 2^64 of lanes [lane0, lane0+lanes), comps x limbs -> canonical (after a uint64 reduce-scatter)
+__global__ void reduce_lanes_kernel(View v, u32 lane0, u32 comps, u32 limbs, u32 n,
+                                    const PrimeConst* __restrict__ pc, u32 cpr) {
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, lane = lane0 + rest / comps;
+  const PrimeConst P = pc[lb];
+  u64* s = v.limb(lane, comp, lb, n);
+  for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
+    s[t] = reduce104(u128{s[t], 0}, P.p, P.mu104);
+}
+
+cudaError_t launch_reduce_lanes(View v, u32 lane0, u32 lanes, u32 comps, u32 limbs, u32 n, const PrimeConst* pc,
+                                cudaStream_t st) {
+  const u32 cpr = chunks_of(n);
+  const size_t g = (size_t)lanes * comps * limbs * cpr;
+  if (!g) return cudaSuccess;
+  reduce_lanes_kernel<<<(unsigned)g, kThreads, 0, st>>>(v, lane0, comps, limbs, n, pc, cpr);
   return cudaGetLastError();
 }
 
@@ -418,11 +441,11 @@ cudaError_t launch_basis_convert(const ConvPlanDev* plan, const u64* hat_tables,
   if (!total) return cudaSuccess;
   const unsigned grid = (unsigned)((total + 255) / 256);
   switch (k) {
-    case 1: basis_convert_kernel<1><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
-    case 2: basis_convert_kernel<2><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
-    case 3: basis_convert_kernel<3><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
-    case 4: basis_convert_kernel<4><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
-    default: basis_convert_kernel<0><<<grid, 256, 0, st>>>(plan, hat_tables, io, n, k, m); break;
+    case 1: basis_convert_kernel<1><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
+    case 2: basis_convert_kernel<2><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
+    case 3: basis_convert_kernel<3><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
+    case 4: basis_convert_kernel<4><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
+    default: basis_convert_kernel<0><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
   }
   return cudaGetLastError();
 }
@@ -450,31 +473,31 @@ cudaError_t launch_weight_rowkeys(u64* out, u32 wlanes, u32 limbs, u64 seed, u64
   return cudaGetLastError();
 }
 
-cudaError_t launch_pmult_acc(View acc, u32 acc_lane0, View x, u32 x_lane0, u32 tg, u32 c_in, u32 c_out,
-                             u32 o_off, u32 w_cout, u32 limbs, u32 n, const u64* w_rowkeys,
-                             const PrimeConst* pc, cudaStream_t st) {
-  if (n < kPmTx) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)tg * c_in * 2 * kPmTx * sizeof(u64);
-  const unsigned grid = limbs * (n / kPmTx);
-  if (!grid) return cudaSuccess;
+cudaError_t launch_pmult_acc(const PmultArgs& a, const PrimeConst* pc, cudaStream_t st) {
+  if (a.n < kPmTx) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)a.tg * a.c_in * 2 * kPmTx * sizeof(u64);
+  const unsigned grid = a.limbs * (a.n / kPmTx);
+  if (!grid || !a.c_in || !a.c_out) return cudaSuccess;
 #define AEGIS_PM(TGV)                                                                          \
   case TGV: {                                                                                  \
     auto kern = pmult_kernel<TGV>;                                                             \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    kern<<<grid, kPmTx * kPmGroups, smem, st>>>(acc, acc_lane0, x, x_lane0, c_in, c_out, o_off, w_cout, limbs, n, w_rowkeys, pc); \
+    kern<<<grid, kPmTx * kPmGroups, smem, st>>>(a, pc);                                        \
     break;                                                                                     \
   }
-  switch (tg) {
+  switch (a.tg) {
     AEGIS_PM(1)
     AEGIS_PM(2)
     AEGIS_PM(3)
     AEGIS_PM(4)
     default: {
       // more token groups than the templated cases: process in groups of 4
-      for (u32 t0 = 0; t0 < tg; t0 += 4) {
-        const u32 tt = tg - t0 < 4 ? tg - t0 : 4;
-        cudaError_t e = launch_pmult_acc(acc, acc_lane0 + t0 * c_out, x, x_lane0 + t0 * c_in, tt, c_in,
-                                         c_out, o_off, w_cout, limbs, n, w_rowkeys, pc, st);
+      for (u32 t0 = 0; t0 < a.tg; t0 += 4) {
+        PmultArgs b = a;
+        b.tg = a.tg - t0 < 4 ? a.tg - t0 : 4;
+        b.acc_lane0 = a.acc_lane0 + t0 * a.acc_tstride;
+        b.x_lane0 = a.x_lane0 + t0 * a.x_tstride;
+        cudaError_t e = launch_pmult_acc(b, pc, st);
         if (e != cudaSuccess) return e;
       }
       return cudaSuccess;

@@ -73,9 +73,17 @@ cudaError_t launch_cadd(View out, u32 out_lane0, View a, LaneMap ma, View b, Lan
 
 // Bundled PCMM step (he_ir.hpp:360-371):
 // acc[t*c_out+o] += sum_ci X[t*c_in+ci] * W[ci*c_out+o], W generated in-kernel.
-cudaError_t launch_pmult_acc(View acc, u32 acc_lane0, View x, u32 x_lane0, u32 tg, u32 c_in, u32 c_out,
-                             u32 o_off, u32 w_cout, u32 limbs, u32 n, const u64* w_rowkeys,
-                             const PrimeConst* pc, cudaStream_t st);
+// acc lane (t, o) = acc_lane0 + t*acc_tstride + o ; X lane (t, ci) = x_lane0 + t*x_tstride + ci ;
+// weight lane = (ci_off + ci) * w_cout + o_off + o   (t < tg, ci < c_in, o < c_out)
+struct PmultArgs {
+  View acc;
+  u32 acc_lane0, acc_tstride;
+  View x;
+  u32 x_lane0, x_tstride;
+  u32 tg, c_in, c_out, ci_off, o_off, w_cout, limbs, n;
+  const u64* rowkeys;
+};
+cudaError_t launch_pmult_acc(const PmultArgs& a, const PrimeConst* pc, cudaStream_t st);
 cudaError_t launch_weight_rowkeys(u64* out, u32 wlanes, u32 limbs, u64 seed, u64 bundle,
                                   cudaStream_t st);
 
@@ -115,7 +123,11 @@ cudaError_t launch_copy(View dst, u32 dst_lane0, View src, LaneMap sm, u32 nlane
                         u32 src_limb0, u32 n, cudaStream_t st);
 
 // DESIGN.md §2.4 content hash over lanes x comps x limbs (dense positions)
-cudaError_t launch_hash(View v, u32 lanes, u32 comps, u32 limbs, u32 n, unsigned long long* out,
+// (lanes [lane0, lane0+lanes) only; positions use absolute lane indices so shard
+// hashes sum to the unsharded hash)
+cudaError_t launch_hash(View v, u32 lane0, u32 lanes, u32 comps, u32 limbs, u32 n, unsigned long long* out,
                         cudaStream_t st);
+cudaError_t launch_reduce_lanes(View v, u32 lane0, u32 lanes, u32 comps, u32 limbs, u32 n, const PrimeConst* pc,
+                                cudaStream_t st);
 
 }  // namespace aegis

@@ -51,9 +51,19 @@ def upload(c, arr):
     return b
 
 
+@pytest.fixture(params=[0, 1], ids=["int", "f64"])
+def ntt_impl(request):
+    from paper_2604_03425_b200 import _lib
+    lib = _lib.load()
+    old = lib.aegis_ntt_impl(-1)
+    lib.aegis_ntt_impl(request.param)
+    yield request.param
+    lib.aegis_ntt_impl(old)
+
+
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("logn", [4, 5, 10, 12, 13, 16, 17])
-def test_ntt_forward_inverse(logn):
+def test_ntt_forward_inverse(logn, ntt_impl):
     c, o = ctx(logn), orc(logn)
     rng = np.random.default_rng(logn)
     level = 3 if logn >= 16 else 6
@@ -69,7 +79,7 @@ def test_ntt_forward_inverse(logn):
     assert (b.download() == x).all()
 
 
-def test_ntt_all_primes_production():
+def test_ntt_all_primes_production(ntt_impl):
     """inverse(forward(x)) == x on every one of the 64 primes at N = 2^16, and
     bit-exact vs the oracle on a sample of them (including the specials)."""
     c, o = ctx(16), orc(16)
@@ -155,17 +165,18 @@ def test_basis_convert_random(logn, k):
 
 
 @pytest.mark.parametrize("logn,level", [(4, 1), (4, 5), (10, 3), (10, 9), (12, 17), (16, 6)])
-def test_keyswitch(logn, level):
+@pytest.mark.parametrize("key", [0, 1007])
+def test_keyswitch(logn, level, key):
     c, o = ctx(logn), orc(logn)
     n = 1 << logn
     rng = np.random.default_rng(level)
     x = rand_bundle(rng, 2, 2, level, n)
     bi = upload(c, x)
     bo = c.bundle(2, 2, level)
-    c.keyswitch(bo, bi, 1, level, 1007)
+    c.keyswitch(bo, bi, 1, level, key)
     got = bo.download()
     for ln in range(2):
-        o0, o1 = o.keyswitch(x[ln, 1], level, 1007)
+        o0, o1 = o.keyswitch(x[ln, 1], level, key)
         assert (got[ln, 0] == o0).all() and (got[ln, 1] == o1).all()
 
 
@@ -331,6 +342,66 @@ def test_graph_parity_small(name, logn, golden_dir):
     # the GPU's own lowering produces the same graph and the same residues
     g2 = c.graph(kind=1 if name.startswith("ffn") else 0, tokens=int(name.split("_t")[1]))
     assert (g2.run(hashes=True) == h_gpu).all()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_execution_matches(world, golden_dir):
+    """Token-group sharding run rank by rank on one GPU: the
+    per-rank bundle hashes (owned lanes only) sum to the unsharded hashes.
+    world = 4 on 2 token groups exercises the PCMM reduce-scatter: the ranks
+    run concurrently in threads, each with its own context, and the reducer
+    hook sums the partner buffers on the device."""
+    import threading
+    import torch
+    from paper_2604_03425_b200 import Context
+    path = golden_graph("block_n11_t32", golden_dir)
+    base = ctx(11).load_graph(path).run(hashes=True)
+    ctxs = [Context(log_n=11) for _ in range(world)]
+    graphs = [c_.load_graph(path) for c_ in ctxs]
+    for r, g in enumerate(graphs):
+        g.set_shard(world, r)
+    m = graphs[0].shard_info()["ranks_per_group"]
+    bar = threading.Barrier(world)
+    bufs = {}
+
+    def reducer(rank):
+        def fn(ptr, words, group):
+            from paper_2604_03425_b200.dist import _CudaWords
+            part = rank % m
+            full = torch.as_tensor(_CudaWords(ptr, words * m), device="cuda")
+            bufs[rank] = full
+            bar.wait()
+            peers = [bufs[group * m + q] for q in range(m)]
+            s = sum(p[part * words:(part + 1) * words].clone() for p in peers)
+            torch.cuda.synchronize()
+            bar.wait()
+            full[part * words:(part + 1) * words].copy_(s)
+            torch.cuda.synchronize()
+            bar.wait()
+        return fn
+
+    out = [None] * world
+    errs = []
+
+    def work(r):
+        try:
+            graphs[r].set_reducer(reducer(r))
+            out[r] = graphs[r].run(hashes=True)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    total = np.zeros_like(base)
+    for h in out:
+        total = total + h  # uint64 wrap-around == the hash's mod 2^64 sum
+    bad = np.nonzero(total != base)[0]
+    assert len(bad) == 0, f"{len(bad)} bundles differ, first {bad[:5]}"
 
 
 @pytest.mark.slow
