@@ -33,25 +33,27 @@ namespace {
 
 thread_local std::string g_create_err;
 
+// context-free calls (ctx == NULL) report through aegis_last_error(NULL)
 template <class F>
 int guard(aegis_ctx* ctx, F&& f) {
+  std::string& err = ctx ? ctx->err : g_create_err;
   try {
     f();
     return AEGIS_OK;
   } catch (const Error& e) {
-    if (ctx) ctx->err = e.what();
+    err = e.what();
     return e.code;
   } catch (const std::invalid_argument& e) {
-    if (ctx) ctx->err = e.what();
+    err = e.what();
     return AEGIS_EINVAL;
   } catch (const std::logic_error& e) {
-    if (ctx) ctx->err = e.what();
+    err = e.what();
     return AEGIS_ELOGIC;
   } catch (const std::bad_alloc& e) {
-    if (ctx) ctx->err = "host allocation failed";
+    err = "host allocation failed";
     return AEGIS_EOOM;
   } catch (const std::exception& e) {
-    if (ctx) ctx->err = e.what();
+    err = e.what();
     return AEGIS_ECUDA;
   }
 }
@@ -107,6 +109,7 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.reduce = g->reduce;
   opt.reduce_user = g->reduce_user;
   opt.hoist = g->hoist != 0;
+  c.trim();
   c.peak_bytes = c.live_bytes;
   aegis::Executor ex(c, g->g, opt);
   ex.run();

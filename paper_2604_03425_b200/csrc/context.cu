@@ -187,6 +187,14 @@ u64* Context::alloc(size_t words) {
   void* p = nullptr;
   if (!words) words = 1;
   cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), stream);
+  if (e == cudaErrorMemoryAllocation) {
+    // the pool keeps freed blocks cached (release threshold = max); hand the
+    // idle ones back to the device and retry once before giving up
+    cudaGetLastError();
+    cudaStreamSynchronize(stream);
+    cudaMemPoolTrimTo(pool_, 0);
+    e = cudaMallocAsync(&p, words * sizeof(u64), stream);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error(e == cudaErrorMemoryAllocation ? AEGIS_EOOM : AEGIS_ECUDA,

@@ -63,6 +63,11 @@ class Context {
   // memory (stream ordered)
   u64* alloc(size_t words);
   void release(void* p);
+  // return idle pool memory to the device (synchronises the stream)
+  void trim() {
+    cudaStreamSynchronize(stream);
+    cudaMemPoolTrimTo(pool_, 0);
+  }
   size_t live_bytes = 0, peak_bytes = 0;
 
   Bundle* new_bundle(u32 lanes, u32 comps, u32 level, bool zero);

@@ -129,8 +129,9 @@ size_t Executor::hoist_budget(size_t out_bytes) {
   size_t fr = 0, total = 0;
   cudaMemGetInfo(&fr, &total);
   const size_t reserved = c.live_bytes + c.total_key_bytes() + ((size_t)c.n * 4 * 16 * kNumExt);
-  const size_t cap = (size_t)(0.92 * (double)total);
-  const size_t margin = out_bytes + ((size_t)6 << 30);
+  const size_t cap = (size_t)(0.90 * (double)total);
+  // room for this op's output, the next few bundles and the key-switch workspaces
+  const size_t margin = 2 * out_bytes + ((size_t)8 << 30);
   return cap > reserved + margin ? cap - reserved - margin : 0;
 }
 

@@ -344,20 +344,21 @@ def test_graph_parity_small(name, logn, golden_dir):
     assert (g2.run(hashes=True) == h_gpu).all()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_execution_matches(world, golden_dir):
-    """Token-group sharding run rank by rank on one GPU: the
-    per-rank bundle hashes (owned lanes only) sum to the unsharded hashes.
-    world = 4 on 2 token groups exercises the PCMM reduce-scatter: the ranks
-    run concurrently in threads, each with its own context, and the reducer
-    hook sums the partner buffers on the device."""
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_execution_matches(world):
+    """Token-group sharding on one GPU: the per-rank bundle
+    hashes (owned lanes only) sum to the unsharded hashes.  N = 2^11, T = 64
+    gives 4 token groups (score lanes >= output lanes, so attention stays
+    inside a group as at T = 2048, N = 2^16); world = 8 puts 2 ranks on each
+    group and exercises the PCMM reduce-scatter: the ranks run concurrently in
+    threads, each with its own context, and the reducer hook sums the partner
+    buffers on the device."""
     import threading
     import torch
     from paper_2604_03425_b200 import Context
-    path = golden_graph("block_n11_t32", golden_dir)
-    base = ctx(11).load_graph(path).run(hashes=True)
+    base = ctx(11).graph(kind=0, tokens=64).run(hashes=True)
     ctxs = [Context(log_n=11) for _ in range(world)]
-    graphs = [c_.load_graph(path) for c_ in ctxs]
+    graphs = [c_.graph(kind=0, tokens=64) for c_ in ctxs]
     for r, g in enumerate(graphs):
         g.set_shard(world, r)
     m = graphs[0].shard_info()["ranks_per_group"]

@@ -94,6 +94,21 @@ def test_shard_rejects_bad_world():
         g.set_shard(6, 0)  # neither divides nor is a multiple of 4 token groups
 
 
+def test_shard_detects_cross_group_coupling():
+    """When score lanes < A.V output lanes the reference's A.V reads wrapped
+    score lanes (he_ir.hpp:533-541) from another token
+    group: token sharding would need a collective there, so it is refused
+    with the reference's logic_error type.  BASELINE configs (T=2048, N=2^16)
+    never wrap."""
+    from paper_2604_03425_b200 import LogicError
+    g = plan_graph(log_n=11, tokens=32, layers=1, kind=0)
+    with pytest.raises(LogicError, match="token groups"):
+        g.set_shard(2, 0)
+    g = plan_graph(log_n=11, tokens=64, layers=1, kind=0)
+    g.set_shard(8, 3)
+    assert g.shard_info() == {"tg_total": 4, "tg_lo": 1, "tg_hi": 2, "ranks_per_group": 2, "part": 1}
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
