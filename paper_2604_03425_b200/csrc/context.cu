@@ -197,9 +197,13 @@ u64* Context::alloc(size_t words) {
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
     throw Error(e == cudaErrorMemoryAllocation ? AEGIS_EOOM : AEGIS_ECUDA,
                 std::string("device allocation of ") + std::to_string(words * 8) + " bytes failed: " +
-                    cudaGetErrorString(e));
+                    cudaGetErrorString(e) + " (bundles live " + std::to_string(live_bytes >> 20) + " MiB, keys " +
+                    std::to_string(total_key_bytes() >> 20) + " MiB, device free " + std::to_string(fr >> 20) +
+                    " of " + std::to_string(tot >> 20) + " MiB)");
   }
   return static_cast<u64*>(p);
 }

@@ -25,6 +25,7 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
   cur_comps.assign(nb, 0);
   zero_first.assign(nb, 0);
   partial.assign(nb, 0);
+  donated.assign(nb, 0);
   last_use.assign(nb, -1);
   std::vector<char> seen(nb, 0);
   for (size_t i = 0; i < nb; ++i) alloc_comps[i] = g.bundles[i].components;
@@ -45,8 +46,8 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
 Executor::~Executor() {
   for (auto& gr : groups)
     if (gr.ext) c.release(gr.ext);
-  for (auto* b : buf)
-    if (b) c.free_bundle(b);
+  for (size_t i = 0; i < buf.size(); ++i)
+    if (buf[i] && !donated[i]) c.free_bundle(buf[i]);
 }
 
 Bundle& Executor::get(u32 id) {
@@ -66,6 +67,10 @@ Bundle& Executor::input(const hp::LaneSlice& s) {
 
 void Executor::retire(u32 id) {
   if (!buf[id]) return;
+  if (donated[id]) {  // storage now belongs to the op's output bundle
+    buf[id] = nullptr;
+    return;
+  }
   if (partial[id]) reduce_partial(id);
   const Bundle& b = *buf[id];
   const hp::CtBundle& cb = g.bundles[id];
@@ -274,6 +279,40 @@ void Executor::reduce_partial(u32 b) {
   }
 }
 
+// Buffer donation: an element-wise op (Rescale, non-accumulating CAdd) whose
+// first operand dies here and covers the output lane-for-lane writes its result
+// into the operand's storage (same strides, fewer limbs used).  Both kernels
+// read each position before writing it, so in-place is exact; it removes the
+// 53 GB score copy at T = 2048.
+void Executor::donate(const hp::HeOp& op, int64_t i) {
+  using K = hp::HeOpKind;
+  if (op.kind != K::kRescale && !(op.kind == K::kCAdd && !op.accumulate)) return;
+  if (buf[op.out.bundle] || op.ins.empty()) return;
+  const hp::LaneSlice& s = op.ins[0];
+  if (s.bundle == op.out.bundle || last_use[s.bundle] != i || !buf[s.bundle]) return;
+  const hp::CtBundle& ob = g.bundles[op.out.bundle];
+  Bundle& in = *buf[s.bundle];
+  if (s.lane != 0 || op.out.lane != 0 || s.lane_count != ob.lanes || op.out.lane_count != ob.lanes ||
+      in.lanes != ob.lanes || in.level < ob.level || in.level > ob.level + 1 ||
+      in.comps != std::max<u32>(2, alloc_comps[op.out.bundle]))
+    return;  // only when the donated storage is (nearly) the output's own size
+  for (size_t k = 1; k < op.ins.size(); ++k)  // a second operand must not alias differently
+    if (op.ins[k].bundle == s.bundle && (op.ins[k].lane != 0 || op.ins[k].lane_count != ob.lanes)) return;
+  if (partial[s.bundle]) reduce_partial(s.bundle);
+  if (o.d_hash) {  // the operand dies now: hash it before it is overwritten
+    std::vector<std::pair<u32, u32>> runs =
+        o.shard ? o.shard->runs(s.bundle, 0, in.lanes) : std::vector<std::pair<u32, u32>>{{0, in.lanes}};
+    for (auto [a, e] : runs) {
+      AEGIS_CHECK_CUDA(launch_hash(in.view(), a, e - a, cur_comps[s.bundle], g.bundles[s.bundle].level, c.n,
+                                   o.d_hash + s.bundle, c.stream));
+      c.count();
+    }
+  }
+  buf[op.out.bundle] = buf[s.bundle];  // same allocation, operand strides
+  donated[s.bundle] = 1;               // still readable by this op; never freed or hashed again
+  cur_comps[op.out.bundle] = 2;
+}
+
 void Executor::step(const hp::HeOp& op, int64_t i) {
   using K = hp::HeOpKind;
   const u32 L = op.use_level;
@@ -285,6 +324,7 @@ void Executor::step(const hp::HeOp& op, int64_t i) {
     return;
   }
   if (partial[op.out.bundle]) reduce_partial(op.out.bundle);
+  donate(op, i);
   const u32 n = op.out.lane_count;
   for (auto [rs, re] : out_runs(op)) {
     for (u32 pos = rs; pos < re;) {
@@ -367,7 +407,12 @@ void Executor::run() {
   const int64_t nops = o.max_ops < 0 ? (int64_t)g.ops.size() : std::min<int64_t>(o.max_ops, (int64_t)g.ops.size());
   for (int64_t i = 0; i < nops; ++i) {
     const hp::HeOp& op = g.ops[i];
-    step(op, i);
+    try {
+      step(op, i);
+    } catch (const Error& e) {
+      throw Error(e.code, std::string(e.what()) + " [op " + std::to_string(i) + " -> " +
+                              g.bundles[op.out.bundle].tag + "]");
+    }
     std::set<u32> touched{op.out.bundle};
     for (auto& s : op.ins) touched.insert(s.bundle);
     for (u32 b : touched)

@@ -56,6 +56,7 @@ class Executor {
   void pmult(const heplan::HeOp& op);
   void rot_run(const heplan::HeOp& op, int64_t i, u32 r0, u32 len);
   void reduce_partial(u32 bundle);
+  void donate(const heplan::HeOp& op, int64_t i);
   std::vector<std::pair<u32, u32>> out_runs(const heplan::HeOp& op) const;
   static LaneMap sub_map(const heplan::LaneSlice& s, u32 n, u32 pos, u32 len);
   u32 wrap_end(const heplan::HeOp& op, u32 pos, u32 end) const;
@@ -65,7 +66,7 @@ class Executor {
   RunOptions o;
   std::vector<Bundle*> buf;
   std::vector<u32> alloc_comps, cur_comps;
-  std::vector<char> zero_first, partial;
+  std::vector<char> zero_first, partial, donated;
   std::vector<int64_t> last_use;
   std::vector<Group> groups;
   std::vector<int> group_of;
