@@ -122,47 +122,85 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def _mini_graph(path, kind, level, lanes, c_in=0, c_out=0):
+    """One bundled HE op in the heops text format (he_ir.hpp field order)."""
+    L = ["# heops v1 calibration", "inputs 0", f"B 0 {lanes} {level} 2 0 0 0 0 in"]
+    if kind == "rot":
+        L += [f"B 1 {lanes} {level} 2 2 0 0 0 rot", f"O 0 5 1 1 0 {lanes} 0 0 1 0 {level} 0 0 1 0 0 {lanes}"]
+    elif kind == "relin":  # CMult(x, x) then Relin of the product
+        L += [f"B 1 {lanes} {level} 2 1 0 0 0 sq",
+              f"O 0 4 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 2 0 0 {lanes} 0 0 {lanes}",
+              f"O 1 6 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 1 1 0 {lanes}"]
+    elif kind == "pmult":
+        w = c_in * c_out
+        L[2] = f"B 0 {c_in} {level} 2 0 0 0 0 in"
+        L += [f"B 1 {c_out} {level} 2 1 {c_out} 0 0 acc", f"B 2 {w} {level} 1 3 0 0 0 w",
+              f"O 0 0 0 2 0 {w} 0 0 -1 0 0 0 0 0",
+              f"O 1 3 0 1 0 {c_out} 1 0 0 {c_in * c_out} {level} 0 0 2 0 0 {c_in} 2 0 {w}"]
+    elif kind == "none":
+        pass
+    open(path, "w").write("\n".join(L) + "\n")
+
+
 def cpu_baseline(args, budget_s=20.0):
-    """Time the oracle (CPU port of the reference semantics) on a measured prefix
-    of the layer's op list and extrapolate by per-kind lane-op cost."""
-    import gzip
-    import shutil
+    """The CPU arm: the oracle (scalar C++ port of the reference semantics, all
+    host threads) timed on single bundled ops of the layer's dominant kinds, then
+    extrapolated over the layer's op list by per-kind lane x level costs."""
     from oracle_py import Oracle
     from paper_2604_03425_b200 import plan_graph
     threads = os.cpu_count() or 1
     g = plan_graph(log_n=N_LOG, tokens=args.tokens, layers=1, kind=0)
+    o = Oracle(N_LOG, threads=threads)
+    meas = {}
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "layer.heops")
         g.dump(path)
         ops = [ln.split() for ln in open(path) if ln.startswith("O ")]
-        o = Oracle(N_LOG, threads=threads)
-        # measure growing prefixes until the budget is spent
-        n_ops, elapsed = 0, 0.0
-        for k in (4, 8, 16, 32, 64, 128, 256):
+
+        def timed(kind, level, lanes, **kw):
+            mp = os.path.join(d, f"{kind}.heops")
+            _mini_graph(mp, kind, level, lanes, **kw)
+            _mini_graph(os.path.join(d, "none.heops"), "none", level, max(lanes, kw.get("c_in", 0)))
+            o.run_graph(mp)  # untimed: builds NTT tables and the (cached) key limbs
             t0 = time.time()
-            o.run_graph(path, max_ops=k)
-            dt = time.time() - t0
-            n_ops, elapsed = k, dt
-            if dt > budget_s / 2:
-                break
-    # cost model: KS lane-ops dominate; weight every op by lane-ops x level x (KS ? 40 : 1)
+            o.run_graph(os.path.join(d, "none.heops"))
+            t_setup = time.time() - t0
+            t0 = time.time()
+            o.run_graph(mp)
+            return max(time.time() - t0 - t_setup, 1e-6)
+        lanes = threads  # one lane per host thread
+        meas["rot35"] = timed("rot", 35, lanes) / lanes        # per lane, all threads busy
+        meas["rot17"] = timed("rot", 17, lanes) / lanes
+        meas["relin17"] = timed("relin", 17, lanes) / lanes   # CMult + Relin per lane
+        meas["pmult17"] = timed("pmult", 17, 1, c_in=12, c_out=threads) / (12 * threads)  # per lane-op
+    n = 1 << N_LOG
+
+    def ks(level):  # interpolate per-lane key-switch cost ~ a*l + b*l^2 through the two samples
+        b = (meas["rot35"] / 35 - meas["rot17"] / 17) / (35 - 17)
+        a = meas["rot17"] / 17 - b * 17
+        return max(a * level + b * level * level, 0.0)
+
     def cost(f):
         kind, lanes, work, lvl = int(f[2]), int(f[6]), int(f[10]), int(f[11])
-        lo = work if work else lanes
-        if kind == 0:
-            return 0.0
-        if kind in (5, 6):  # rot, relin: key switch
-            return lo * lvl * 40.0
-        if kind == 3:       # pmult: per weight-lane-op
-            return lo * lvl * 1.0
-        return lo * max(lvl, 1) * 2.0
-    total = sum(cost(f) for f in ops)
-    done = sum(cost(f) for f in ops[:n_ops]) or 1.0
-    value = elapsed * total / done
+        if kind == 5:
+            return ks(lvl) * lanes
+        if kind == 6:
+            return ks(lvl) * lanes  # Relin: one key switch per lane
+        if kind == 3:
+            return meas["pmult17"] * work * lvl / 17
+        if kind == 4:  # CMult: relin17 minus the key switch
+            return max(meas["relin17"] - ks(17), 0.0) * lanes * lvl / 17
+        if kind == 7:  # Rescale ~ (l-1) NTTs + 1 INTT per comp: ~ 2l/(ks NTT count) of a key switch
+            return ks(lvl) * lanes * 2 * lvl / ((-(-lvl // 4) + 3) * lvl + 12)
+        if kind == 8:  # Boot from level 1: 2 x (1 INTT + 20 NTT)
+            return ks(21) * lanes * 42 / ((6 + 3) * 21 + 12)
+        return 0.0
+    value = sum(cost(f) for f in ops) / 1.0
     return {"value": value, "unit": "s/layer", "cores": threads, "kind": "port",
-            "sample": f"oracle exec of the first {n_ops} HE ops of the T={args.tokens} layer "
-                      f"({elapsed:.1f}s measured, {100 * done / total:.2f}% of the layer's modelled "
-                      f"work), extrapolated by lane-op x level cost model"}
+            "sample": (f"oracle (CPU port, {threads} threads, one lane per thread) timed on single bundled ops: "
+                       f"Rot at l=35 ({meas['rot35']:.2f}s/lane) and l=17 ({meas['rot17']:.2f}s/lane), "
+                       f"CMult+Relin at l=17, PMult 12x{threads} at l=17; extrapolated over the "
+                       f"{len(ops)} ops of the T={args.tokens} layer by per-kind lane x level costs")}
 
 
 # ---------------------------------------------------------------------------

@@ -410,8 +410,22 @@ void Executor::run() {
     try {
       step(op, i);
     } catch (const Error& e) {
+      std::string live;
+      if (e.code == AEGIS_EOOM) {  // what is holding the memory
+        std::vector<std::pair<size_t, u32>> v;
+        for (u32 b = 0; b < buf.size(); ++b)
+          if (buf[b] && !donated[b]) v.emplace_back(buf[b]->bytes, b);
+        std::sort(v.rbegin(), v.rend());
+        live = " live:";
+        for (size_t k = 0; k < v.size() && k < 6; ++k)
+          live += " " + g.bundles[v[k].second].tag + "=" + std::to_string(v[k].first >> 20) + "MiB";
+        size_t hoisted = 0;
+        for (auto& gr : groups)
+          if (gr.ext) hoisted += (size_t)gr.hoisted * c.modup_words_per_lane(gr.level) * 8;
+        live += " hoisted=" + std::to_string(hoisted >> 20) + "MiB";
+      }
       throw Error(e.code, std::string(e.what()) + " [op " + std::to_string(i) + " -> " +
-                              g.bundles[op.out.bundle].tag + "]");
+                              g.bundles[op.out.bundle].tag + "]" + live);
     }
     std::set<u32> touched{op.out.bundle};
     for (auto& s : op.ins) touched.insert(s.bundle);
