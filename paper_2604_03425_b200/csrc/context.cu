@@ -587,25 +587,20 @@ void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im
   if (L < 2) throw Error(AEGIS_EINVAL, "level underflow: cannot rescale below level 1");
   if (im.count != lanes) throw Error(AEGIS_ELOGIC, "rescale operand lanes must match");
   const u32 m = L - 1;
-  u64* last = alloc((size_t)2 * lanes * n);
-  u64* conv = alloc((size_t)2 * lanes * m * n);
-  // last limb of every (lane, comp) -> [lane][comp][n]
-  AEGIS_CHECK_CUDA(launch_copy(View{last, lanes, 2, 1}, 0, in.view(), im, lanes, 2, 1, L - 1, n, stream));
-  count();
-  ntt(last, n, 2 * lanes, {0}, {L - 1}, true);
+  // lanes in batches so the workspace stays ~1 GB (a T=2048 score tensor is 50 GB)
+  const size_t per_lane = (size_t)2 * n * (1 + m);
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)1 << 30) / (per_lane * 8)));
+  u64* last = alloc((size_t)2 * B * n);
+  u64* conv = alloc((size_t)2 * B * m * n);
   std::vector<u32> off(m), ext(m);
   for (u32 i = 0; i < m; ++i) off[i] = ext[i] = i;
-  basis_convert(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * lanes);
-  ntt(conv, (size_t)m * n, 2 * lanes, off, ext, false);
   FinishIO f;
   std::memset(&f, 0, sizeof(f));
-  f.x = in.view().limb(im.lane0, 0, 0, n);
   f.x_lane = (size_t)in.comps * in.level * n;
   f.x_comp = (size_t)in.level * n;
   f.y = conv;
   f.y_lane = (size_t)2 * m * n;
   f.y_comp = (size_t)m * n;
-  f.out = out.view().limb(out_lane, 0, 0, n);
   f.out_lane = (size_t)out.comps * out.level * n;
   f.out_comp = (size_t)out.level * n;
   f.comps = 2;
@@ -617,8 +612,21 @@ void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im
     f.f[i] = h_inv(ql % q, q);
     f.f_p[i] = h_shoup(f.f[i], q);
   }
-  AEGIS_CHECK_CUDA(launch_finish(f, lanes, n, d_pc, stream));
-  count();
+  for (u32 l0 = 0; l0 < lanes; l0 += B) {
+    const u32 nb = std::min(B, lanes - l0);
+    // last limb of every (lane, comp) -> [lane][comp][n], Intt, centred lift to q_0..q_{L-2}, Ntt
+    AEGIS_CHECK_CUDA(launch_copy(View{last, nb, 2, 1}, 0, in.view(), LaneMap{im.lane0 + l0, nb}, nb, 2, 1, L - 1, n,
+                                 stream));
+    count();
+    ntt(last, n, 2 * nb, {0}, {L - 1}, true);
+    basis_convert(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * nb);
+    ntt(conv, (size_t)m * n, 2 * nb, off, ext, false);
+    // out_i = (x_i - r_i) * q_{L-1}^{-1}   (div_round on the centred value, rns_math.hpp:196-202)
+    f.x = in.view().limb(im.lane0 + l0, 0, 0, n);
+    f.out = out.view().limb(out_lane + l0, 0, 0, n);
+    AEGIS_CHECK_CUDA(launch_finish(f, nb, n, d_pc, stream));
+    count();
+  }
   release(last);
   release(conv);
 }

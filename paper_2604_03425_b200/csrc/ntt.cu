@@ -126,6 +126,16 @@ __device__ __forceinline__ double mulmod_f64(double y, double w, double wp, doub
   const double q = rint(y * wp);
   return fma(-q, p, h) + l;
 }
+// same, rounding with the 1.5 * 2^52 magic constant on the DFMA pipe (no XU
+// FRND); valid while |y * w / p| < 2^51 -- true for the forward transform,
+// whose lazy values stay below ~25 p < 2^51 with p < 2^46.
+__device__ __forceinline__ double mulmod_f64_fast(double y, double w, double wp, double p) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double h = y * w;
+  const double l = fma(y, w, -h);
+  const double q = fma(y, wp, kMagic) - kMagic;
+  return fma(-q, p, h) + l;
+}
 __device__ __forceinline__ double reduce_f64(double x, double p, double pinv) {
   return fma(-rint(x * pinv), p, x);  // |result| <= p/2 + 1
 }
@@ -142,7 +152,7 @@ struct F64Arith {
   double p, pinv;
   const NttScale* sc;
   __device__ __forceinline__ void ct(T& a, T& b, Tw w) const {
-    const double t = mulmod_f64(b, w.x, w.y, p);
+    const double t = mulmod_f64_fast(b, w.x, w.y, p);
     const double x = a;
     a = x + t;
     b = x - t;
@@ -175,18 +185,23 @@ __device__ __forceinline__ void ct_round(typename A::T* sp, u32 tau, int s0, u32
   const u32 tau_lo = tau & ((1u << lo_bits) - 1);
   const u32 tau_hi = tau >> lo_bits;
   const u32 base = tau_lo | (tau_hi << (lo_bits + R));
+  // issue every twiddle load of the round up front (2^R - 1 independent
+  // 128-bit loads in flight) instead of one dependent load per butterfly
+  typename A::Tw wv[(1 << R) - 1];
+#pragma unroll
+  for (int sg = 0; sg < R; ++sg)
+#pragma unroll
+    for (int q = 0; q < (1 << sg); ++q) wv[(1 << sg) - 1 + q] = tw[(t0 << (s0 + sg)) + (tau_hi << sg) + q];
   typename A::T x[1 << R];
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) x[v] = sp[pad_idx(base | ((u32)v << lo_bits))];
 #pragma unroll
   for (int sg = 0; sg < R; ++sg) {
-    const int s = s0 + sg;
     const int half = 1 << (R - sg - 1);
 #pragma unroll
     for (int v = 0; v < (1 << R); ++v) {
       if (v & half) continue;
-      const u32 i = (tau_hi << sg) | ((u32)v >> (R - sg));
-      ar.ct(x[v], x[v + half], tw[(t0 << s) + i]);
+      ar.ct(x[v], x[v + half], wv[(1 << sg) - 1 + (v >> (R - sg))]);
     }
   }
 #pragma unroll
@@ -207,6 +222,12 @@ __device__ __forceinline__ void gs_round(typename A::T* sp, u32 tau, int s0, u32
   const u32 tau_lo = tau & ((1u << lo_bits) - 1);
   const u32 tau_hi = tau >> lo_bits;
   const u32 base = tau_lo | (tau_hi << (lo_bits + R));
+  typename A::Tw wv[(1 << R) - 1];  // all twiddle loads of the round in flight at once
+#pragma unroll
+  for (int sg = 0; sg < R; ++sg)
+#pragma unroll
+    for (int q = 0; q < (1 << sg); ++q)
+      if (!(last && s0 + sg == 0)) wv[(1 << sg) - 1 + q] = tw[(t0 << (s0 + sg)) + (tau_hi << sg) + q];
   typename A::T x[1 << R];
 #pragma unroll
   for (int v = 0; v < (1 << R); ++v) x[v] = sp[pad_idx(base | ((u32)v << lo_bits))];
@@ -219,9 +240,8 @@ __device__ __forceinline__ void gs_round(typename A::T* sp, u32 tau, int s0, u32
 #pragma unroll
     for (int v = 0; v < (1 << R); ++v) {
       if (v & half) continue;
-      const u32 i = (tau_hi << sg) | ((u32)v >> (R - sg));
       if (scale) ar.gs_scale(x[v], x[v + half], bound);
-      else ar.gs(x[v], x[v + half], tw[(t0 << s) + i], bound);
+      else ar.gs(x[v], x[v + half], wv[(1 << sg) - 1 + (v >> (R - sg))], bound);
     }
   }
   if (!last) {
@@ -236,7 +256,7 @@ __device__ __forceinline__ void gs_round(typename A::T* sp, u32 tau, int s0, u32
 //   forward : pass A (canonical -> lazy), pass B (lazy -> canonical)
 //   inverse : pass B (canonical -> lazy), pass A (lazy -> canonical)
 template <int LOGM, int MODE, bool INV, int IMPL>
-__global__ void __launch_bounds__(256) ntt_pass_kernel(const NttLaunch L, int kA, int kB,
+__global__ void __launch_bounds__(256, 3) ntt_pass_kernel(const NttLaunch L, int kA, int kB,
                                                        int subs_per_cta, int scale_last) {
   using C = SubCfg<LOGM>;
   using A = typename std::conditional<IMPL == kNttF64, F64Arith, IntArith>::type;
