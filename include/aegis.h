@@ -156,6 +156,9 @@ int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* t
                            uint32_t* ranks_per_group, uint32_t* part);
 /* hoisted ModUp across the rotations of one source (bit-exact; default on) */
 int aegis_graph_set_hoisting(aegis_graph* g, int enable);
+/* per-op device times (CUDA events around every HeOp) of the next runs */
+int aegis_graph_set_profiling(aegis_graph* g, int enable);
+int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t* n);
 /* bytes copied host->device / device->host by the last aegis_graph_run_host */
 int aegis_graph_io_bytes(const aegis_graph* g, uint64_t* h2d, uint64_t* d2h);
 /* Execute ops [0, max_ops) (all if < 0).  Bundles are allocated at first write

@@ -288,6 +288,17 @@ class Graph:
     def set_hoisting(self, enable):
         self.lib.aegis_graph_set_hoisting(self.h, 1 if enable else 0)
 
+    def set_profiling(self, enable):
+        self.lib.aegis_graph_set_profiling(self.h, 1 if enable else 0)
+
+    def op_times(self):
+        n = ctypes.c_uint64()
+        self.lib.aegis_graph_op_times(self.h, None, 0, ctypes.byref(n))
+        a = np.zeros(n.value, dtype=np.float32)
+        self.lib.aegis_graph_op_times(self.h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n.value,
+                                      ctypes.byref(n))
+        return a
+
     def io_bytes(self):
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         self.lib.aegis_graph_io_bytes(self.h, ctypes.byref(a), ctypes.byref(b))

@@ -88,6 +88,8 @@ struct aegis_graph {
   void* reduce_user = nullptr;
   int hoist = 1;
   uint64_t h2d = 0, d2h = 0;
+  bool profile = false;
+  std::vector<float> op_ms;
 };
 
 namespace {
@@ -109,6 +111,7 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.reduce = g->reduce;
   opt.reduce_user = g->reduce_user;
   opt.hoist = g->hoist != 0;
+  if (g->profile) opt.op_ms = &g->op_ms;
   c.trim();
   c.peak_bytes = c.live_bytes;
   aegis::Executor ex(c, g->g, opt);
@@ -538,6 +541,17 @@ int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* t
   if (tg_hi) *tg_hi = s ? s->tg_hi : tg;
   if (ranks_per_group) *ranks_per_group = s ? s->m : 1;
   if (part) *part = s ? s->part : 0;
+  return AEGIS_OK;
+}
+int aegis_graph_set_profiling(aegis_graph* g, int enable) {
+  if (!g) return AEGIS_EINVAL;
+  g->profile = enable != 0;
+  return AEGIS_OK;
+}
+int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t* n) {
+  if (!g) return AEGIS_EINVAL;
+  for (size_t i = 0; i < g->op_ms.size() && i < cap; ++i) ms[i] = g->op_ms[i];
+  if (n) *n = g->op_ms.size();
   return AEGIS_OK;
 }
 int aegis_graph_set_hoisting(aegis_graph* g, int enable) {

@@ -405,10 +405,17 @@ void Executor::run() {
   }
   if (o.host_out && !g.ops.empty()) final_bundle = g.ops.back().out.bundle;
   const int64_t nops = o.max_ops < 0 ? (int64_t)g.ops.size() : std::min<int64_t>(o.max_ops, (int64_t)g.ops.size());
+  std::vector<cudaEvent_t> ev;
+  if (o.op_ms) {
+    ev.resize(nops + 1);
+    for (auto& e : ev) AEGIS_CHECK_CUDA(cudaEventCreate(&e));
+    AEGIS_CHECK_CUDA(cudaEventRecord(ev[0], c.stream));
+  }
   for (int64_t i = 0; i < nops; ++i) {
     const hp::HeOp& op = g.ops[i];
     try {
       step(op, i);
+      if (o.op_ms) AEGIS_CHECK_CUDA(cudaEventRecord(ev[i + 1], c.stream));
     } catch (const Error& e) {
       std::string live;
       if (e.code == AEGIS_EOOM) {  // what is holding the memory
@@ -438,6 +445,12 @@ void Executor::run() {
       c.release(gr.ext);
       gr.ext = nullptr;
     }
+  if (o.op_ms) {
+    AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.stream));
+    o.op_ms->assign(nops, 0.0f);
+    for (int64_t i = 0; i < nops; ++i) cudaEventElapsedTime(&(*o.op_ms)[i], ev[i], ev[i + 1]);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
 }
 
 }  // namespace aegis

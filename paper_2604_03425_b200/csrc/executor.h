@@ -26,6 +26,7 @@ struct RunOptions {
   ReduceFn reduce = nullptr;
   void* reduce_user = nullptr;
   bool hoist = true;
+  std::vector<float>* op_ms = nullptr;  // if set: per-op device time (CUDA events)
 };
 
 class Executor {
