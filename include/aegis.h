@@ -59,8 +59,9 @@ int aegis_sync(aegis_ctx* ctx);
 uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t ext_index); /* <60 main, >=60 special */
 /* count of kernels this context launched (for the bench's gpu_launches claim) */
 uint64_t aegis_launch_count(const aegis_ctx* ctx);
-/* NTT butterfly arithmetic: 0 = 64-bit integer Shoup, 1 = exact FP64 (default).
- * impl < 0 only queries.  Returns the active implementation. */
+/* NTT butterfly arithmetic: 0 = 64-bit integer Shoup, 1 = exact FP64 (default;
+ * N = 2^16 uses the direct-access v2 passes), 2 = FP64 through the generic
+ * passes.  impl < 0 only queries.  Returns the active implementation. */
 int aegis_ntt_impl(int impl);
 
 /* ---- bundles (CtBundle, he_ir.hpp:57-74) --------------------------------- */

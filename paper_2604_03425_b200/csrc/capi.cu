@@ -153,8 +153,14 @@ int aegis_sync(aegis_ctx* ctx) {
 uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t e) { return e < aegis::kNumExt ? ctx->c->prime(e) : 0; }
 uint64_t aegis_launch_count(const aegis_ctx* ctx) { return ctx ? ctx->c->launches : 0; }
 int aegis_ntt_impl(int impl) {
-  if (impl == aegis::kNttInt || impl == aegis::kNttF64) aegis::g_ntt_impl = impl;
-  return aegis::g_ntt_impl;
+  if (impl == aegis::kNttInt || impl == aegis::kNttF64) {
+    aegis::g_ntt_impl = impl;
+    aegis::g_ntt_v2 = 1;
+  } else if (impl == 2) {  // FP64 butterflies through the generic (v1) passes
+    aegis::g_ntt_impl = aegis::kNttF64;
+    aegis::g_ntt_v2 = 0;
+  }
+  return aegis::g_ntt_impl == aegis::kNttF64 && !aegis::g_ntt_v2 ? 2 : aegis::g_ntt_impl;
 }
 
 int aegis_bundle_alloc(aegis_ctx* ctx, uint32_t lanes, uint32_t comps, uint32_t level, aegis_bundle** out) {

@@ -93,8 +93,13 @@ Context::Context(const aegis_params& prm, int dev) {
   // per prime: int fwd, int inv, f64 fwd, f64 inv
   AEGIS_CHECK_CUDA(cudaMalloc(&d_twiddles_, (size_t)kNumExt * 4 * tab_words * sizeof(u64)));
   std::vector<u64> hf(tab_words), hi(tab_words), pw(n), pwi(n);
-  std::vector<double> ff(tab_words), fi(tab_words);
+  std::vector<double> ff(tab_words), fi(tab_words), fw(n), iw(n);
+  AEGIS_CHECK_CUDA(cudaMalloc(&d_twd_, (size_t)kNumExt * 2 * n * sizeof(double)));
+  const size_t blob_words = log_n == 16 ? (size_t)16 * kNttBlobTile : 0;
+  std::vector<double> fblob(blob_words), iblob(blob_words);
+  if (blob_words) AEGIS_CHECK_CUDA(cudaMalloc(&d_blob_, (size_t)kNumExt * 2 * blob_words * sizeof(double)));
   if (const char* impl = std::getenv("AEGIS_NTT_IMPL")) g_ntt_impl = std::string(impl) == "int" ? kNttInt : kNttF64;
+  if (const char* v2 = std::getenv("AEGIS_NTT_V2")) g_ntt_v2 = std::string(v2) != "0";
   for (u32 e = 0; e < kNumExt; ++e) {
     const u64 p = primes_[e];
     pc[e].p = p;
@@ -125,6 +130,23 @@ Context::Context(const aegis_params& prm, int dev) {
       ff[2 * i + 1] = (double)pw[r] / (double)p;
       fi[2 * i] = (double)pwi[r];
       fi[2 * i + 1] = (double)pwi[r] / (double)p;
+      fw[i] = (double)pw[r];
+      iw[i] = (double)pwi[r];
+    }
+    double* fwd_w = d_twd_ + (size_t)e * 2 * n;
+    AEGIS_CHECK_CUDA(cudaMemcpy(fwd_w, fw.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+    AEGIS_CHECK_CUDA(cudaMemcpy(fwd_w + n, iw.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+    tw[e].fw = fwd_w;
+    tw[e].iw = fwd_w + n;
+    tw[e].fb = tw[e].ib = nullptr;
+    if (blob_words) {
+      ntt_build_blob(fw.data(), fblob.data());
+      ntt_build_blob(iw.data(), iblob.data());
+      double* bf = d_blob_ + (size_t)e * 2 * blob_words;
+      AEGIS_CHECK_CUDA(cudaMemcpy(bf, fblob.data(), blob_words * 8, cudaMemcpyHostToDevice));
+      AEGIS_CHECK_CUDA(cudaMemcpy(bf + blob_words, iblob.data(), blob_words * 8, cudaMemcpyHostToDevice));
+      tw[e].fb = bf;
+      tw[e].ib = bf + blob_words;
     }
     u64* fdev = d_twiddles_ + (size_t)e * 4 * tab_words;
     u64* idev = fdev + tab_words;
@@ -174,6 +196,8 @@ Context::~Context() {
   for (auto& kv : keys_) cudaFree(kv.second);
   for (auto& kv : plans_) cudaFree(kv.second.dev);
   cudaFree(d_twiddles_);
+  cudaFree(d_twd_);
+  cudaFree(d_blob_);
   cudaFree(d_pc);
   cudaFree(d_tw);
   cudaFree(d_scale);

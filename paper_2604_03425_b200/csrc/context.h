@@ -136,6 +136,8 @@ class Context {
  private:
   std::vector<u64> primes_;
   u64* d_twiddles_ = nullptr;
+  double* d_twd_ = nullptr;  // w-only FP64 twiddles [ext][fwd|inv][n]
+  double* d_blob_ = nullptr; // N = 2^16 pass-B twiddle blobs [ext][fwd|inv][16 tiles]
   std::map<std::vector<u32>, Plan> plans_;
   std::map<u64, u64*> keys_;
   u32* d_key_slot_ext_ = nullptr;  // key slot -> ext prime

@@ -36,6 +36,7 @@
 namespace aegis {
 
 int g_ntt_impl = kNttF64;
+int g_ntt_v2 = 1;
 
 namespace {
 
@@ -390,6 +391,308 @@ cudaError_t dispatch_pass(int logm, const NttLaunch& L, int kA, int kB, u32 rows
   }
 }
 
+// ---------------------------------------------------------------------------
+// v2: N = 2^16 FP64 passes (256 x 256) with direct-to-register global access.
+//
+// A CTA owns 16 sub-transforms of 256 points; each of its 256 threads holds
+// 16 elements and runs two radix-16 rounds (stages 0-3, 4-7) with one SMEM
+// exchange between them.  The thread -> (sub, tau) mapping is chosen per pass
+// so that the round whose element pattern is "tau + 16 v" (pass B) or whose
+// sub index is the column (pass A) touches global memory directly with
+// 128-byte coalesced rows: all 16 loads of a thread are independent and in
+// flight together (no SMEM staging, one exposed latency per tile).  Only the
+// forward pass-B store and the inverse pass-B load (pattern "16 tau + v" on
+// contiguous memory) are staged through SMEM.  Rounding uses the 1.5 * 2^52
+// magic constant everywhere (no XU FRND).  Row order is slot-major so CTAs
+// running together share one prime's twiddle table in L2.
+// ---------------------------------------------------------------------------
+namespace v2 {
+
+constexpr int kStride = 273;  // 256 + 16 + 1 padded words per sub-transform
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+// Pass-B twiddle blob (built by ntt_build_blob, one contiguous block per tile
+// so a single TMA bulk copy stages it): per sub, round-2 twiddles stored
+// [sg][q][tau] in 17-word rows (the 16 threads of a sub read one row per
+// (sg, q): conflict free), then the 15 round-1 twiddles (half-warp broadcast).
+constexpr int kTwRow = 17;
+__device__ __host__ __forceinline__ int tw2_off(int sg, int q) { return ((1 << sg) - 1 + q) * kTwRow; }
+constexpr int kTw1 = 15 * kTwRow;
+
+__device__ __forceinline__ double rnd(double x) { return (x + kMagic) - kMagic; }
+// y * w mod p, exact, result in about [-1.5p, 1.5p] (q may be off by one: wp = w * (1/p))
+__device__ __forceinline__ double mm(double y, double w, double wp, double p) {
+  const double h = y * w;
+  const double l = fma(y, w, -h);
+  const double q = fma(y, wp, kMagic) - kMagic;
+  return fma(-q, p, h) + l;
+}
+__device__ __forceinline__ double red(double x, double p, double pinv) { return fma(-rnd(x * pinv), p, x); }
+__device__ __forceinline__ u64 canon(double x, double p, double pinv) {
+  double r = red(x, p, pinv);
+  r = r < 0.0 ? r + p : r;
+  r = r >= p ? r - p : r;
+  return (u64)__double_as_longlong(r + kTwo52) & 0xFFFFFFFFFFFFFULL;
+}
+
+struct Row {
+  u64* ptr;
+  const double* tw;
+  const double* blob;
+  const NttScale* sc;
+};
+
+// slot-major row order: consecutive CTAs share a prime (twiddle table in L2)
+__device__ __forceinline__ Row row_of(const NttLaunch& L, u32 row, bool inv) {
+  const u32 slot = row / L.nlanes;
+  const u32 lane = row - slot * L.nlanes;
+  Row r;
+  r.ptr = L.base + (size_t)lane * L.lane_stride + (size_t)L.slot_off[slot] * L.n;
+  const u32 pr = L.prime[slot];
+  r.tw = inv ? L.tw[pr].iw : L.tw[pr].fw;
+  r.blob = inv ? L.tw[pr].ib : L.tw[pr].fb;
+  r.sc = L.scale + pr;
+  return r;
+}
+
+// Radix-16 rounds.  TW(sg, q) returns the twiddle of stage sg, group q.
+template <class TW>
+__device__ __forceinline__ void ct16(double (&x)[16], TW tw, double p, double pinv) {
+#pragma unroll
+  for (int sg = 0; sg < 4; ++sg) {
+    const int half = 8 >> sg;
+#pragma unroll
+    for (int q = 0; q < (1 << sg); ++q) {
+      const double w = tw(sg, q), wp = w * pinv;
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const int v = q * 2 * half + j;
+        const double t = mm(x[v + half], w, wp, p);
+        const double a = x[v];
+        x[v] = a + t;
+        x[v + half] = a - t;
+      }
+    }
+  }
+}
+
+// GS stages sg = 3..0; SCALE folds N^{-1} into the stage with sg == 0
+template <bool SCALE, class TW>
+__device__ __forceinline__ void gs16(double (&x)[16], TW tw, double p, double pinv, const NttScale* sc) {
+#pragma unroll
+  for (int sg = 3; sg >= 0; --sg) {
+    const int half = 8 >> sg;
+#pragma unroll
+    for (int q = 0; q < (1 << sg); ++q) {
+      double w = 0.0, wp = 0.0;
+      if (!(SCALE && sg == 0)) {
+        w = tw(sg, q);
+        wp = w * pinv;
+      }
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const int v = q * 2 * half + j;
+        const double a = x[v], b = x[v + half];
+        if (SCALE && sg == 0) {
+          x[v] = mm(a + b, sc->n_inv_d, sc->n_inv_wp, p);
+          x[v + half] = mm(a - b, sc->w1n_d, sc->w1n_wp, p);
+        } else {
+          x[v] = a + b;
+          x[v + half] = mm(a - b, w, wp, p);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double dbits(u64 v) { return __longlong_as_double((long long)v); }
+__device__ __forceinline__ u64 bitsd(double v) { return (u64)__double_as_longlong(v); }
+
+// global twiddle of round S0 at (t0, th): tw[(t0 << (S0+sg)) + (th << sg) + q]
+template <int S0>
+struct GTw {
+  const double* __restrict__ tw;
+  u32 t0, th;
+  __device__ __forceinline__ double operator()(int sg, int q) const {
+    return __ldg(tw + (t0 << (S0 + sg)) + (th << sg) + q);
+  }
+};
+// blob twiddles of this thread's sub (round 2: per tau; round 1: broadcast)
+struct BTw2 {
+  const double* sp;  // sub base + tau
+  __device__ __forceinline__ double operator()(int sg, int q) const { return sp[tw2_off(sg, q)]; }
+};
+struct BTw1 {
+  const double* sp;  // sub base
+  __device__ __forceinline__ double operator()(int sg, int q) const { return sp[kTw1 + (1 << sg) - 1 + q]; }
+};
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+// thread 0: init the mbarrier and start the TMA bulk copy of this tile's blob
+__device__ __forceinline__ void blob_issue(u64* mbar, double* dst, const double* src) {
+  if (threadIdx.x == 0) {
+    const u32 bar = smem_u32(mbar);
+    constexpr u32 bytes = (u32)(kNttBlobTile * sizeof(double));
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void blob_wait(u64* mbar) {
+  const u32 bar = smem_u32(mbar);
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 P, [%0], 0;\n @!P bra WAIT_%=;\n}\n" ::"r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void st256(u64* p, u64 a, u64 b, u64 c, u64 d) {
+  asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+__device__ __forceinline__ void ld256(const u64* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
+// forward pass A: columns c = chunk*16 + lo, thread tau = hi.  canonical in, lazy out.
+__global__ void __launch_bounds__(256, 3) fwd_a(const NttLaunch L) {
+  __shared__ double sm[16 * kStride];
+  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
+  const Row r = row_of(L, row, false);
+  const double p = r.sc->pd, pinv = r.sc->pinv;
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  u64* col = r.ptr + chunk * 16 + lo;
+  double x[16];
+  u64 raw[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) raw[v] = col[(size_t)(hi + 16 * v) << 8];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
+  ct16(x, GTw<0>{r.tw, 1, 0}, p, pinv);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sm[lo * kStride + hi + 17 * v] = x[v];
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + 17 * hi + v];
+  ct16(x, GTw<4>{r.tw, 1, hi}, p, pinv);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
+}
+
+// forward pass B: block b = chunk*16 + hi (256 contiguous), tau = lo.  lazy in,
+// canonical out (each thread writes its 16 contiguous outputs as 4 x 32 B).
+__global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
+  extern __shared__ double dyn[];
+  __shared__ u64 mbar;
+  double* sm = dyn;                     // 16 * kStride
+  double* stw = dyn + 16 * kStride;     // one tile blob
+  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
+  const Row r = row_of(L, row, false);
+  blob_issue(&mbar, stw, r.blob + (size_t)chunk * kNttBlobTile);
+  const double p = r.sc->pd, pinv = r.sc->pinv;
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  u64* blk = r.ptr + (size_t)(chunk * 16 + hi) * 256;
+  double x[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = dbits(blk[lo + 16 * v]);
+  __syncthreads();  // mbarrier initialised
+  blob_wait(&mbar);
+  const double* sb = stw + hi * kNttBlobSub;
+  ct16(x, BTw1{sb}, p, pinv);
+  double* sp = sm + hi * kStride;
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = x[v];
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[17 * lo + v];
+  ct16(x, BTw2{sb + lo}, p, pinv);
+  u64* o = blk + 16 * lo;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    st256(o + 4 * k, canon(x[4 * k], p, pinv), canon(x[4 * k + 1], p, pinv), canon(x[4 * k + 2], p, pinv),
+          canon(x[4 * k + 3], p, pinv));
+}
+
+// inverse pass B (first): canonical in (4 x 32 B per thread), lazy out.
+__global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
+  extern __shared__ double dyn[];
+  __shared__ u64 mbar;
+  double* sm = dyn;
+  double* stw = dyn + 16 * kStride;
+  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
+  const Row r = row_of(L, row, true);
+  blob_issue(&mbar, stw, r.blob + (size_t)chunk * kNttBlobTile);
+  const double p = r.sc->pd, pinv = r.sc->pinv;
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  u64* blk = r.ptr + (size_t)(chunk * 16 + hi) * 256;
+  u64 raw[16];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ld256(blk + 16 * lo + 4 * k, raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]);
+  double x[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
+  __syncthreads();
+  blob_wait(&mbar);
+  const double* sb = stw + hi * kNttBlobSub;
+  gs16<false>(x, BTw2{sb + lo}, p, pinv, r.sc);
+  double* sp = sm + hi * kStride;
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[17 * lo + v] = red(x[v], p, pinv);
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[lo + 17 * v];
+  gs16<false>(x, BTw1{sb}, p, pinv, r.sc);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) blk[lo + 16 * v] = bitsd(red(x[v], p, pinv));
+}
+
+// inverse pass A (second): columns c = chunk*16 + lo, tau = hi; lazy in, canonical out, N^{-1} folded.
+__global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
+  __shared__ double sm[16 * kStride];
+  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
+  const Row r = row_of(L, row, true);
+  const double p = r.sc->pd, pinv = r.sc->pinv;
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  u64* col = r.ptr + chunk * 16 + lo;
+  double x[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = dbits(col[(size_t)(16 * hi + v) << 8]);
+  gs16<false>(x, GTw<4>{r.tw, 1, hi}, p, pinv, r.sc);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sm[lo * kStride + 17 * hi + v] = red(x[v], p, pinv);
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + hi + 17 * v];
+  gs16<true>(x, GTw<0>{r.tw, 1, 0}, p, pinv, r.sc);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) col[(size_t)(hi + 16 * v) << 8] = canon(x[v], p, pinv);
+}
+
+constexpr size_t kSmemB = (size_t)(16 * kStride + kNttBlobTile) * sizeof(double);
+
+cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(fwd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
+    cudaFuncSetAttribute(inv_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
+    init = true;
+  }
+  const u32 rows = L.nlanes * L.nslots;
+  const dim3 grid(rows * 16), block(256);
+  if (!inverse) {
+    fwd_a<<<grid, block, 0, st>>>(L);
+    fwd_b<<<grid, block, kSmemB, st>>>(L);
+  } else {
+    inv_b<<<grid, block, kSmemB, st>>>(L);
+    inv_a<<<grid, block, 0, st>>>(L);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace v2
+
 template <int IMPL>
 cudaError_t run_impl(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st) {
   const u32 rows = L.nlanes * L.nslots;
@@ -407,8 +710,23 @@ cudaError_t run_impl(const NttLaunch& L, int log_n, bool inverse, cudaStream_t s
 
 }  // namespace
 
+void ntt_build_blob(const double* tab, double* blob) {
+  for (int c = 0; c < 16; ++c)
+    for (int b = 0; b < 16; ++b) {
+      double* d = blob + (size_t)c * kNttBlobTile + (size_t)b * kNttBlobSub;
+      const unsigned t0 = 256 + 16 * c + b;
+      for (int sg = 0; sg < 4; ++sg)
+        for (int q = 0; q < (1 << sg); ++q) {
+          for (int tau = 0; tau < 16; ++tau) d[v2::tw2_off(sg, q) + tau] = tab[(t0 << (4 + sg)) + (tau << sg) + q];
+          d[v2::tw2_off(sg, q) + 16] = 0.0;
+          d[v2::kTw1 + (1 << sg) - 1 + q] = tab[(t0 << sg) + q];
+        }
+    }
+}
+
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st) {
   if (L.nlanes * L.nslots == 0) return cudaSuccess;
+  if (log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2) return v2::run(L, inverse, st);
   return g_ntt_impl == kNttF64 ? run_impl<kNttF64>(L, log_n, inverse, st) : run_impl<kNttInt>(L, log_n, inverse, st);
 }
 

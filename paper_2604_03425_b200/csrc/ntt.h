@@ -9,6 +9,10 @@ struct PrimeTw {
   const ulonglong2* inv;  // N entries : psi^-brv(i)                 (rns_math.hpp:60)
   const double2* fwd64;   // N entries (w, w/p) as doubles (FP64 butterflies)
   const double2* inv64;
+  const double* fw;       // N entries w as doubles (v2 passes: w/p is formed at use)
+  const double* iw;
+  const double* fb;       // N = 2^16 only: pass-B twiddle blobs per tile (see ntt.cu v2)
+  const double* ib;
   u64 p;
 };
 struct NttScale {
@@ -22,6 +26,7 @@ struct NttScale {
 // Butterfly arithmetic of the NTT passes.
 enum NttImpl : int { kNttInt = 0, kNttF64 = 1 };
 extern int g_ntt_impl;  // selected at context creation (AEGIS_NTT_IMPL=int|f64)
+extern int g_ntt_v2;    // N = 2^16 FP64 passes with direct global access (AEGIS_NTT_V2=0 disables)
 
 constexpr int kMaxSlots = 96;
 
@@ -36,6 +41,13 @@ struct NttLaunch {
   const PrimeTw* tw;       // device, indexed by ext prime
   const NttScale* scale;   // device, indexed by ext prime
 };
+
+// pass-B twiddle blob of one 16-sub tile at N = 2^16 (ntt.cu v2):
+// per sub 15 rows x 17 doubles of round-2 twiddles + 15 round-1 twiddles
+constexpr int kNttBlobSub = 15 * 17 + 15;
+constexpr int kNttBlobTile = 16 * kNttBlobSub;
+// build the fwd (or inv) blob of one prime from its bit-reversed power table tab[0..2^16)
+void ntt_build_blob(const double* tab, double* blob);
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st);
 

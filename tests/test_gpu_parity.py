@@ -51,7 +51,7 @@ def upload(c, arr):
     return b
 
 
-@pytest.fixture(params=[0, 1], ids=["int", "f64"])
+@pytest.fixture(params=[0, 1, 2], ids=["int", "f64", "f64v1"])
 def ntt_impl(request):
     from paper_2604_03425_b200 import _lib
     lib = _lib.load()
