@@ -203,6 +203,7 @@ Context::~Context() {
   cudaFree(d_scale);
   cudaFree(d_ident);
   cudaFree(d_key_slot_ext_);
+  arena_.reset();
   cudaStreamDestroy(stream);
   cudaStreamDestroy(comm);
 }
@@ -210,29 +211,54 @@ Context::~Context() {
 u64* Context::alloc(size_t words) {
   void* p = nullptr;
   if (!words) words = 1;
-  cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), stream);
+  const size_t bytes = words * sizeof(u64);
+  if (bytes >= kArenaMin) {
+    if (!arena_) arena_.reset(new Arena(device));
+    p = arena_->alloc(bytes);
+    if (!p) {
+      // idle pool blocks (small allocations) hold physical memory too
+      cudaStreamSynchronize(stream);
+      cudaMemPoolTrimTo(pool_, 0);
+      p = arena_->alloc(bytes);
+    }
+    if (p) return static_cast<u64*>(p);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    throw Error(AEGIS_EOOM, std::string("device allocation of ") + std::to_string(bytes) +
+                                " bytes failed (arena mapped " + std::to_string(arena_->mapped() >> 20) +
+                                " MiB, in use " + std::to_string(arena_->in_use() >> 20) + " MiB, largest free " +
+                                std::to_string(arena_->largest_free() >> 20) + " MiB; bundles live " +
+                                std::to_string(live_bytes >> 20) + " MiB, keys " + std::to_string(total_key_bytes() >> 20) +
+                                " MiB, device free " + std::to_string(fr >> 20) + " of " + std::to_string(tot >> 20) +
+                                " MiB)");
+  }
+  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
   if (e == cudaErrorMemoryAllocation) {
-    // the pool keeps freed blocks cached (release threshold = max); hand the
-    // idle ones back to the device and retry once before giving up
     cudaGetLastError();
     cudaStreamSynchronize(stream);
     cudaMemPoolTrimTo(pool_, 0);
-    e = cudaMallocAsync(&p, words * sizeof(u64), stream);
+    if (arena_) arena_->trim();
+    e = cudaMallocAsync(&p, bytes, stream);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
     throw Error(e == cudaErrorMemoryAllocation ? AEGIS_EOOM : AEGIS_ECUDA,
-                std::string("device allocation of ") + std::to_string(words * 8) + " bytes failed: " +
-                    cudaGetErrorString(e) + " (bundles live " + std::to_string(live_bytes >> 20) + " MiB, keys " +
-                    std::to_string(total_key_bytes() >> 20) + " MiB, device free " + std::to_string(fr >> 20) +
-                    " of " + std::to_string(tot >> 20) + " MiB)");
+                std::string("device allocation of ") + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
   }
   return static_cast<u64*>(p);
 }
 void Context::release(void* p) {
-  if (p) cudaFreeAsync(p, stream);
+  if (!p) return;
+  if (arena_ && arena_->owns(p)) {
+    arena_->free(p);  // reuse is ordered after this stream's pending work
+    return;
+  }
+  cudaFreeAsync(p, stream);
+}
+void Context::trim() {
+  cudaStreamSynchronize(stream);
+  cudaMemPoolTrimTo(pool_, 0);
+  if (arena_) arena_->trim();
 }
 
 Bundle* Context::new_bundle(u32 lanes, u32 comps, u32 level, bool zero) {
@@ -432,7 +458,7 @@ Context::KsShape Context::ks_shape(u32 l) const {
 void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
   if (l == 0 || l > chain) throw Error(AEGIS_EINVAL, "key switch level out of range");
   const KsShape S = ks_shape(l);
-  const size_t ext_ls = (size_t)S.dn * S.ns * n;
+  const size_t ext_ls = modup_words_per_lane(l);
   std::vector<u32> main_off(l), main_ext(l);
   for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
   const size_t budget = (size_t)1 << 30;
@@ -447,9 +473,13 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
       const u32 lo = j * kAlpha, hi = std::min(l, lo + kAlpha);
       std::vector<u32> s_off, s_ext, t_off, t_ext;
       for (u32 i = lo; i < hi; ++i) { s_off.push_back(i); s_ext.push_back(i); }
+      // compact layout: digit j stores only its ns - |D_j| target slots
       for (u32 t = 0; t < S.ns; ++t)
-        if (t < lo || t >= hi) { t_off.push_back(t); t_ext.push_back(t < l ? t : kSpecialBase + (t - l)); }
-      u64* ej = ext + (size_t)l0 * ext_ls + (size_t)j * S.ns * n;
+        if (t < lo || t >= hi) {
+          t_off.push_back((u32)t_off.size());
+          t_ext.push_back(t < l ? t : kSpecialBase + (t - l));
+        }
+      u64* ej = ext + (size_t)l0 * ext_ls + (size_t)(j * S.ns - lo) * n;
       basis_convert(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb);
       ntt(ej, ext_ls, nb, t_off, t_ext, false);
     }
@@ -461,7 +491,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
                       const KsOut& o) {
   const KsShape S = ks_shape(l);
   const u32 K = kAlpha, ns = S.ns;
-  const size_t ext_ls = (size_t)S.dn * ns * n, acc_ls = (size_t)2 * ns * n;
+  const size_t ext_ls = modup_words_per_lane(l), acc_ls = (size_t)2 * ns * n;
   std::vector<u32> main_off(l), main_ext(l);
   for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
   const size_t per_lane = (size_t)n * (2 * ns + 2 * (size_t)l);
@@ -533,8 +563,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
 }
 
 void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id, const KsOut& o, u64 galois) {
-  const KsShape S = ks_shape(l);
-  const size_t ext_lane = (size_t)S.dn * S.ns * n;
+  const size_t ext_lane = modup_words_per_lane(l);
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)2 << 30) / (ext_lane * 8)));
   u64* ext = alloc(ext_lane * B);
   const u64* kbase = key(key_id);

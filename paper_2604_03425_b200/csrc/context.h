@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/aegis.h"
+#include "arena.h"
 #include "kernels.h"
 #include "ntt.h"
 #include "shard.h"
@@ -63,11 +64,9 @@ class Context {
   // memory (stream ordered)
   u64* alloc(size_t words);
   void release(void* p);
-  // return idle pool memory to the device (synchronises the stream)
-  void trim() {
-    cudaStreamSynchronize(stream);
-    cudaMemPoolTrimTo(pool_, 0);
-  }
+  // return idle pool / arena memory to the device (synchronises the stream)
+  void trim();
+  static constexpr size_t kArenaMin = (size_t)4 << 20;  // allocations >= this come from the arena
   size_t live_bytes = 0, peak_bytes = 0;
 
   Bundle* new_bundle(u32 lanes, u32 comps, u32 level, bool zero);
@@ -106,8 +105,10 @@ class Context {
     u32 l, ns, dn;
   };
   KsShape ks_shape(u32 l) const;
-  size_t modup_words_per_lane(u32 l) const { return (size_t)ks_shape(l).dn * ks_shape(l).ns * n; }
-  // ext[lane][digit][slot][n] = Ntt(exact lift of Intt(d) digit j to slot t)
+  // compact ModUp output: digit j holds its ns - |D_j| converted slots, at
+  // word offset (j * ns - first prime of D_j) * n  (own-digit slots are read from d)
+  size_t modup_words_per_lane(u32 l) const { return ((size_t)ks_shape(l).dn * ks_shape(l).ns - l) * n; }
+  // ext[lane][digit][compact slot][n] = Ntt(exact lift of Intt(d) digit j to slot t)
   void modup(const u64* d, size_t d_ls, u32 lanes, u32 level, u64* ext);
   void ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 level, const u64* key, u64 galois,
                const KsOut& o);
@@ -142,6 +143,7 @@ class Context {
   std::map<u64, u64*> keys_;
   u32* d_key_slot_ext_ = nullptr;  // key slot -> ext prime
   cudaMemPool_t pool_ = nullptr;
+  std::unique_ptr<Arena> arena_;
 };
 
 }  // namespace aegis

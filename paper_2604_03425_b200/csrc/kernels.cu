@@ -245,7 +245,6 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
   const PrimeConst P = pc[e];
   const u32 ks = io.slot_key[slot];
   const size_t kslot_stride = (size_t)io.key_slots * n;  // per comp
-  const u64* ext = io.ext + (size_t)lane * io.ext_lane_stride + (size_t)slot * n;
   const u64* dd = io.d + (size_t)lane * io.d_lane_stride + (size_t)slot * n;
   u64* a0 = io.acc + (size_t)lane * io.acc_lane_stride + (size_t)slot * n;
   u64* a1 = a0 + (size_t)io.nslots * n;
@@ -253,8 +252,11 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
   for (u32 x = chunk * kChunk + threadIdx.x; x < n && x < (chunk + 1) * kChunk; x += kThreads) {
     Acc3 s0, s1;
     for (u32 j = 0; j < io.dnum; ++j) {
-      const bool own = main_slot && slot >= j * kAlpha && slot < j * kAlpha + kAlpha;
-      const Split v = split24(own ? dd[x] : ext[(size_t)j * io.nslots * n + x]);
+      const u32 lo = j * kAlpha, hi = lo + kAlpha < io.level ? lo + kAlpha : io.level;
+      const bool own = main_slot && slot >= lo && slot < hi;
+      // compact ModUp layout (Context::modup_words_per_lane): digit j at (j*ns - lo)
+      const u32 idx = j * io.nslots - lo + (slot < lo ? slot : slot - (hi - lo));
+      const Split v = split24(own ? dd[x] : io.ext[(size_t)lane * io.ext_lane_stride + (size_t)idx * n + x]);
       const u64* kj = io.key + (size_t)j * 2 * kslot_stride + (size_t)ks * n + x;
       mac24(s0, v, split24(__ldg(kj)));
       mac24(s1, v, split24(__ldg(kj + kslot_stride)));

@@ -32,7 +32,7 @@ def launches(path, out):
         f.write(f"{'kernel':60s} {'launches':>9s} {'total_ms':>10s} {'share':>7s} {'avg_us':>9s}\n")
         for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"{k[:60]:60s} {v[0]:9d} {v[1] / 1e6:10.2f} {100 * v[1] / tot:6.1f}% {v[1] / v[0] / 1e3:9.1f}\n")
-    print(open(out).read())
+
 
 
 METRICS = [
@@ -65,7 +65,7 @@ def full(path, out):
                 if m in h:
                     i = h.index(m)
                     f.write(f"  {m:80s} {r[i]} {units[i]}\n")
-    print(open(out).read())
+
 
 
 if __name__ == "__main__":
