@@ -100,6 +100,8 @@ Context::Context(const aegis_params& prm, int dev) {
   if (blob_words) AEGIS_CHECK_CUDA(cudaMalloc(&d_blob_, (size_t)kNumExt * 2 * blob_words * sizeof(double)));
   if (const char* impl = std::getenv("AEGIS_NTT_IMPL")) g_ntt_impl = std::string(impl) == "int" ? kNttInt : kNttF64;
   if (const char* v2 = std::getenv("AEGIS_NTT_V2")) g_ntt_v2 = std::string(v2) != "0";
+  if (const char* cf = std::getenv("AEGIS_CONV_FUSED")) g_conv_fused = std::string(cf) != "0";
+
   for (u32 e = 0; e < kNumExt; ++e) {
     const u64 p = primes_[e];
     pc[e].p = p;
@@ -330,6 +332,7 @@ const Plan& Context::plan(const std::vector<u32>& src, const std::vector<u32>& d
     h.dst_p[t] = d;
     h.dst_mu[t] = (u64)(((u128h)1 << 104) / d);
     h.b_mod[t] = big_mod(B, d);
+    h.dst_mu96[t] = (u64)(((u128h)1 << 96) / d);
   }
   Plan pl;
   pl.k = k;
@@ -439,6 +442,56 @@ void Context::basis_convert(const u64* src, size_t src_ls, const std::vector<u32
   count();
 }
 
+// Exact conversion of `lanes` source sets followed by the forward NTT of the
+// targets.  At N = 2^16 with <= 4 sources this is the fused path: one prep
+// kernel (sources -> xt in place, overflow counts -> vbuf) and the NTT whose
+// first pass computes the converted values itself (ntt.cu cfwd_a).  The
+// sources are clobbered either way (callers pass scratch limbs).
+void Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
+                       u64* dst, size_t dst_ls, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
+                       u32 lanes, u64* vbuf) {
+  const bool fused = log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2 && g_conv_fused && src_off.size() <= 4 &&
+                     dst_off.size() <= (size_t)kMaxSlots && vbuf != nullptr;
+  if (!fused) {
+    basis_convert(src, src_ls, src_off, src_ext, dst, dst_ls, dst_off, dst_ext, lanes);
+    ntt(dst, dst_ls, lanes, dst_off, dst_ext, false);
+    return;
+  }
+  const Plan& pl = plan(src_ext, dst_ext);
+  ConvIO io;
+  std::memset(&io, 0, sizeof(io));
+  io.src = src;
+  io.src_lane_stride = src_ls;
+  for (size_t i = 0; i < src_off.size(); ++i) io.src_off[i] = src_off[i];
+  AEGIS_CHECK_CUDA(launch_conv_prep(pl.dev, pl.tables, io, vbuf, n, lanes, n, pl.k, pl.m, stream));
+  count();
+  NttLaunch L;
+  std::memset(&L, 0, sizeof(L));
+  L.base = dst;
+  L.lane_stride = dst_ls;
+  L.nlanes = lanes;
+  L.nslots = (u32)dst_off.size();
+  L.n = n;
+  for (size_t i = 0; i < dst_off.size(); ++i) {
+    L.slot_off[i] = dst_off[i];
+    L.prime[i] = (unsigned char)dst_ext[i];
+  }
+  L.tw = d_tw;
+  L.scale = d_scale;
+  NttConvIn c;
+  std::memset(&c, 0, sizeof(c));
+  c.plan = pl.dev;
+  c.hat_tab = pl.tables;
+  c.src = src;
+  c.src_ls = src_ls;
+  for (size_t i = 0; i < src_off.size(); ++i) c.src_off[i] = src_off[i];
+  c.k = pl.k;
+  c.v = vbuf;
+  c.v_ls = n;
+  AEGIS_CHECK_CUDA(ntt_conv_fwd(L, c, stream));
+  count(2);
+}
+
 // ---------------------------------------------------------------------------
 // Hybrid key switching, split so the ModUp can be hoisted:
 //   modup()   Intt(d) -> per digit exact centred lift to Q_l u P -> Ntt
@@ -463,7 +516,8 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
   for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
   const size_t budget = (size_t)1 << 30;
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / ((size_t)l * n * 8)));
-  u64* dc = alloc((size_t)B * l * n);
+  u64* dc = alloc((size_t)B * (l + 1) * n);
+  u64* vbuf = dc + (size_t)B * l * n;
   for (u32 l0 = 0; l0 < lanes; l0 += B) {
     const u32 nb = std::min(B, lanes - l0);
     AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(dc, (size_t)l * n * 8, d + (size_t)l0 * d_ls, d_ls * 8, (size_t)l * n * 8, nb,
@@ -480,8 +534,7 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
           t_ext.push_back(t < l ? t : kSpecialBase + (t - l));
         }
       u64* ej = ext + (size_t)l0 * ext_ls + (size_t)(j * S.ns - lo) * n;
-      basis_convert(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb);
-      ntt(ej, ext_ls, nb, t_off, t_ext, false);
+      conv_ntt(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb, vbuf);
     }
   }
   release(dc);
@@ -497,8 +550,9 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
   const size_t per_lane = (size_t)n * (2 * ns + 2 * (size_t)l);
   const size_t budget = (size_t)1 << 30;
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / (per_lane * 8)));
-  u64* acc = alloc(per_lane * B);                 // [B][2][ns][n]
+  u64* acc = alloc((per_lane + 2 * (size_t)n) * B);  // [B][2][ns][n]
   u64* pcv = acc + (size_t)B * 2 * ns * n;        // [B][2][l][n]
+  u64* vbuf = pcv + (size_t)B * 2 * l * n;        // [2B][n]
   // constants of the finish step: P^{-1} mod q_i
   FinishIO f;
   std::memset(&f, 0, sizeof(f));
@@ -544,8 +598,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
     // ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}
     ntt(acc, acc_ls, nb, p_off, p_ext, true);
     // (lane, comp) pairs are uniform "virtual lanes" of stride ns*n / l*n
-    basis_convert(acc, (size_t)ns * n, ps_off, ps_ext, pcv, (size_t)l * n, main_off, main_ext, 2 * nb);
-    ntt(pcv, (size_t)l * n, 2 * nb, main_off, main_ext, false);
+    conv_ntt(acc, (size_t)ns * n, ps_off, ps_ext, pcv, (size_t)l * n, main_off, main_ext, 2 * nb, vbuf);
     for (u32 c = 0; c < 2; ++c) {
       f.x = acc + (size_t)c * ns * n;
       f.x_lane = acc_ls;
@@ -644,7 +697,8 @@ void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im
   const size_t per_lane = (size_t)2 * n * (1 + m);
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)1 << 30) / (per_lane * 8)));
   u64* last = alloc((size_t)2 * B * n);
-  u64* conv = alloc((size_t)2 * B * m * n);
+  u64* conv = alloc((size_t)2 * B * (m + 1) * n);
+  u64* vbuf = conv + (size_t)2 * B * m * n;
   std::vector<u32> off(m), ext(m);
   for (u32 i = 0; i < m; ++i) off[i] = ext[i] = i;
   FinishIO f;
@@ -672,8 +726,7 @@ void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im
                                  stream));
     count();
     ntt(last, n, 2 * nb, {0}, {L - 1}, true);
-    basis_convert(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * nb);
-    ntt(conv, (size_t)m * n, 2 * nb, off, ext, false);
+    conv_ntt(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * nb, vbuf);
     // out_i = (x_i - r_i) * q_{L-1}^{-1}   (div_round on the centred value, rns_math.hpp:196-202)
     f.x = in.view().limb(im.lane0 + l0, 0, 0, n);
     f.out = out.view().limb(out_lane + l0, 0, 0, n);

@@ -90,6 +90,11 @@ class Context {
   void basis_convert(const u64* src, size_t src_lane_stride, const std::vector<u32>& src_off,
                      const std::vector<u32>& src_ext, u64* dst, size_t dst_lane_stride,
                      const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext, u32 lanes);
+  // exact conversion + forward NTT of the targets (fused at N = 2^16, k <= 4);
+  // clobbers the sources; vbuf: lanes * n words of scratch
+  void conv_ntt(u64* src, size_t src_lane_stride, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
+                u64* dst, size_t dst_lane_stride, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
+                u32 lanes, u64* vbuf);
   // Hybrid key switch (poly_ir.hpp:219-298) of `lanes` polynomials d (level
   // limbs each, NTT domain, lane stride d_ls).  out_c = add_c + KS_c(d).
   struct KsOut {

@@ -8,6 +8,8 @@
 // op touches only the lanes this rank owns; PCMM with several ranks per token
 // group accumulates partial sums that are reduce-scattered before the rescale.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <set>
 
@@ -133,10 +135,13 @@ void Executor::find_hoist_groups() {
 size_t Executor::hoist_budget(size_t out_bytes) {
   size_t fr = 0, total = 0;
   cudaMemGetInfo(&fr, &total);
+  // live bundles (this op's output included: it is allocated before the group
+  // is prepared), keys and tables are resident; keep 6 GB for the CUDA/NCCL
+  // runtime and 8 GB (or one more output, if larger) for the products,
+  // accumulators and key-switch workspaces of the ops inside the group
   const size_t reserved = c.live_bytes + c.total_key_bytes() + ((size_t)c.n * 4 * 16 * kNumExt);
-  const size_t cap = (size_t)(0.90 * (double)total);
-  // room for this op's output, the next few bundles and the key-switch workspaces
-  const size_t margin = 2 * out_bytes + ((size_t)8 << 30);
+  const size_t cap = total > ((size_t)6 << 30) ? total - ((size_t)6 << 30) : 0;
+  const size_t margin = std::max<size_t>((size_t)8 << 30, out_bytes / 4);
   return cap > reserved + margin ? cap - reserved - margin : 0;
 }
 
@@ -162,6 +167,9 @@ void Executor::rot_run(const hp::HeOp& op, int64_t i, u32 pos, u32 len) {
       total += e - s;
     }
     gr.hoisted = (u32)std::min<size_t>(total, hoist_budget(out.bytes) / (per_lane * 8));
+    if (std::getenv("AEGIS_DEBUG"))
+      fprintf(stderr, "[aegis] hoist %s: %u of %u lanes at level %u (%zu MiB/lane, %u rotations)\n",
+              g.bundles[gr.src].tag.c_str(), gr.hoisted, total, L, per_lane * 8 >> 20, gr.size);
     if (gr.hoisted > 0) {
       gr.ext = c.alloc(per_lane * gr.hoisted);
       const size_t in_ls = (size_t)in.comps * in.level * c.n;

@@ -231,6 +231,38 @@ __global__ void __launch_bounds__(256) basis_convert_kernel(const ConvPlanDev* _
   }
 }
 
+// First half of the conversion, once per source set: the
+// sources are replaced in place by xt_i = x_i (B/b_i)^{-1} mod b_i and the
+// overflow count v = round(sum xt_i / b_i) is written to vbuf.  The fused
+// conversion + NTT pass (ntt.cu cfwd_a) then needs only k+1 MACs per target.
+template <int K>
+__global__ void __launch_bounds__(256) conv_prep_kernel(const ConvPlanDev* __restrict__ pl,
+                                                        const u64* __restrict__ hat_tab, ConvIO io, u64* vbuf,
+                                                        size_t v_ls, u32 lanes, u32 n, u32 m) {
+  const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= lanes * n) return;
+  const u32 lane = gid / n, x = gid - lane * n;
+  u64* src = const_cast<u64*>(io.src) + (size_t)lane * io.src_lane_stride + x;
+  u64 xt[K];
+  u64 F_lo = 0, F_hi = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const u64 b = pl->src_p[i];
+    const u64 t = shoup(src[(size_t)io.src_off[i] * n], pl->hat_inv[i], pl->hat_inv_p[i], b);
+    xt[i] = t;
+    const u64 f = t * pl->w_hi[i] + __umul64hi(t, pl->w_lo[i]);
+    F_lo += f;
+    F_hi += F_lo < f;
+  }
+  const u64 half = 1ull << 63;
+  u64 low = F_lo + half;
+  u64 v = F_hi + (low < half);
+  if (low >= (u64)0 - 2ull * K) v = tie_resolve(pl, hat_tab + (size_t)2 * K * m, xt, K, v);
+#pragma unroll
+  for (int i = 0; i < K; ++i) src[(size_t)io.src_off[i] * n] = (xt[i] & 0xFFFFFFull) | ((xt[i] >> 24) << 32);
+  vbuf[(size_t)lane * v_ls + x] = v;  // v <= k < 2^24: already in split form
+}
+
 // ---------------------------------------------------------------------------
 // Key inner product
 // ---------------------------------------------------------------------------
@@ -448,6 +480,21 @@ cudaError_t launch_basis_convert(const ConvPlanDev* plan, const u64* hat_tables,
     case 3: basis_convert_kernel<3><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
     case 4: basis_convert_kernel<4><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
     default: basis_convert_kernel<0><<<grid, 256, 0, st>>>(plan, hat_tables, io, lanes, n, k, m); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, const ConvIO& io, u64* vbuf,
+                             size_t v_ls, u32 lanes, u32 n, u32 k, u32 m, cudaStream_t st) {
+  const size_t total = (size_t)lanes * n;
+  if (!total) return cudaSuccess;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  switch (k) {
+    case 1: conv_prep_kernel<1><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 2: conv_prep_kernel<2><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 3: conv_prep_kernel<3><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 4: conv_prep_kernel<4><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

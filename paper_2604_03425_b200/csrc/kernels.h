@@ -33,6 +33,7 @@ struct ConvPlanDev {
   u64 w_hi[kMaxConv], w_lo[kMaxConv];           // floor(2^128 / b_i)
   u64 dst_p[kMaxConv], dst_mu[kMaxConv];
   u64 b_mod[kMaxConv];                          // B mod d_t
+  u64 dst_mu96[kMaxConv];                       // floor(2^96 / d_t): lazy reduction in ntt.cu cfwd_a
   u32 big_words;
   u64 b_big[kMaxBigWords];                      // B (multiword, little endian)
   // followed in memory by: hat_mod[k][m], hat_mod_p[k][m], hat_big[k][big_words]
@@ -49,6 +50,11 @@ struct ConvIO {
 
 cudaError_t launch_basis_convert(const ConvPlanDev* plan, const u64* hat_tables, const ConvIO& io,
                                  u32 lanes, u32 n, u32 k, u32 m, cudaStream_t st);
+
+// conversion prep (k <= 4): sources -> xt in place, overflow counts -> vbuf[lane * v_ls + x];
+// both written in 24-bit split form (low 24 bits | high bits << 32) for cfwd_a's MACs
+cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, const ConvIO& io, u64* vbuf,
+                             size_t v_ls, u32 lanes, u32 n, u32 k, u32 m, cudaStream_t st);
 
 // rows of a view filled with the DESIGN.md §2.3 PRNG:
 // row key = row_key(seed, tag, a, lane, comp, limb) for every (lane, comp, limb)

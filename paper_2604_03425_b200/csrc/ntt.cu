@@ -29,14 +29,17 @@
 //              B200) and leaves the integer pipes to addressing.
 // The intermediate between the two passes is lazy (raw u64 or raw double bits);
 // only values leaving the transform are canonicalised.
+#include <cstring>
 #include <type_traits>
 
+#include "kernels.h"
 #include "ntt.h"
 
 namespace aegis {
 
 int g_ntt_impl = kNttF64;
 int g_ntt_v2 = 1;
+int g_conv_fused = 1;
 
 namespace {
 
@@ -434,26 +437,6 @@ __device__ __forceinline__ u64 canon(double x, double p, double pinv) {
   return (u64)__double_as_longlong(r + kTwo52) & 0xFFFFFFFFFFFFFULL;
 }
 
-struct Row {
-  u64* ptr;
-  const double* tw;
-  const double* blob;
-  const NttScale* sc;
-};
-
-// slot-major row order: consecutive CTAs share a prime (twiddle table in L2)
-__device__ __forceinline__ Row row_of(const NttLaunch& L, u32 row, bool inv) {
-  const u32 slot = row / L.nlanes;
-  const u32 lane = row - slot * L.nlanes;
-  Row r;
-  r.ptr = L.base + (size_t)lane * L.lane_stride + (size_t)L.slot_off[slot] * L.n;
-  const u32 pr = L.prime[slot];
-  r.tw = inv ? L.tw[pr].iw : L.tw[pr].fw;
-  r.blob = inv ? L.tw[pr].ib : L.tw[pr].fb;
-  r.sc = L.scale + pr;
-  return r;
-}
-
 // Radix-16 rounds.  TW(sg, q) returns the twiddle of stage sg, group q.
 template <class TW>
 __device__ __forceinline__ void ct16(double (&x)[16], TW tw, double p, double pinv) {
@@ -462,11 +445,11 @@ __device__ __forceinline__ void ct16(double (&x)[16], TW tw, double p, double pi
     const int half = 8 >> sg;
 #pragma unroll
     for (int q = 0; q < (1 << sg); ++q) {
-      const double w = tw(sg, q), wp = w * pinv;
+      const double2 wv = tw(sg, q, pinv);
 #pragma unroll
       for (int j = 0; j < half; ++j) {
         const int v = q * 2 * half + j;
-        const double t = mm(x[v + half], w, wp, p);
+        const double t = mm(x[v + half], wv.x, wv.y, p);
         const double a = x[v];
         x[v] = a + t;
         x[v + half] = a - t;
@@ -483,11 +466,8 @@ __device__ __forceinline__ void gs16(double (&x)[16], TW tw, double p, double pi
     const int half = 8 >> sg;
 #pragma unroll
     for (int q = 0; q < (1 << sg); ++q) {
-      double w = 0.0, wp = 0.0;
-      if (!(SCALE && sg == 0)) {
-        w = tw(sg, q);
-        wp = w * pinv;
-      }
+      double2 wv = make_double2(0.0, 0.0);
+      if (!(SCALE && sg == 0)) wv = tw(sg, q, pinv);
 #pragma unroll
       for (int j = 0; j < half; ++j) {
         const int v = q * 2 * half + j;
@@ -497,43 +477,53 @@ __device__ __forceinline__ void gs16(double (&x)[16], TW tw, double p, double pi
           x[v + half] = mm(a - b, sc->w1n_d, sc->w1n_wp, p);
         } else {
           x[v] = a + b;
-          x[v + half] = mm(a - b, w, wp, p);
+          x[v + half] = mm(a - b, wv.x, wv.y, p);
         }
       }
     }
   }
 }
 
+// Rounds with the 15 twiddles of the round preloaded (w only, w/p formed at
+// use): all loads of a round are issued together at its start, so only the
+// first stage waits on them.
+template <int S0>
+__device__ __forceinline__ void load_w(double (&w)[15], const double* __restrict__ tw, u32 t0, u32 th) {
+#pragma unroll
+  for (int sg = 0; sg < 4; ++sg)
+#pragma unroll
+    for (int q = 0; q < (1 << sg); ++q) w[(1 << sg) - 1 + q] = __ldg(tw + (t0 << (S0 + sg)) + (th << sg) + q);
+}
+__device__ __forceinline__ void load_w_blob(double (&w)[15], const double* sp) {
+#pragma unroll
+  for (int sg = 0; sg < 4; ++sg)
+#pragma unroll
+    for (int q = 0; q < (1 << sg); ++q) w[(1 << sg) - 1 + q] = sp[((1 << sg) - 1 + q) * 17];
+}
+struct WArr {
+  const double* w;
+  __device__ __forceinline__ double2 operator()(int sg, int q, double pinv) const {
+    const double t = w[(1 << sg) - 1 + q];
+    return make_double2(t, t * pinv);
+  }
+};
+
 __device__ __forceinline__ double dbits(u64 v) { return __longlong_as_double((long long)v); }
 __device__ __forceinline__ u64 bitsd(double v) { return (u64)__double_as_longlong(v); }
 
-// global twiddle of round S0 at (t0, th): tw[(t0 << (S0+sg)) + (th << sg) + q]
-template <int S0>
-struct GTw {
-  const double* __restrict__ tw;
-  u32 t0, th;
-  __device__ __forceinline__ double operator()(int sg, int q) const {
-    return __ldg(tw + (t0 << (S0 + sg)) + (th << sg) + q);
-  }
-};
-// blob twiddles of this thread's sub (round 2: per tau; round 1: broadcast)
-struct BTw2 {
-  const double* sp;  // sub base + tau
-  __device__ __forceinline__ double operator()(int sg, int q) const { return sp[tw2_off(sg, q)]; }
-};
-struct BTw1 {
-  const double* sp;  // sub base
-  __device__ __forceinline__ double operator()(int sg, int q) const { return sp[kTw1 + (1 << sg) - 1 + q]; }
-};
-
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
-// thread 0: init the mbarrier and start the TMA bulk copy of this tile's blob
+__device__ __forceinline__ void blob_init(u64* mbar) {
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+// thread 0: arm the mbarrier and start the TMA bulk copy of a tile's blob
 __device__ __forceinline__ void blob_issue(u64* mbar, double* dst, const double* src) {
   if (threadIdx.x == 0) {
     const u32 bar = smem_u32(mbar);
     constexpr u32 bytes = (u32)(kNttBlobTile * sizeof(double));
-    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar));
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -542,10 +532,11 @@ __device__ __forceinline__ void blob_issue(u64* mbar, double* dst, const double*
                  : "memory");
   }
 }
-__device__ __forceinline__ void blob_wait(u64* mbar) {
+__device__ __forceinline__ void blob_wait(u64* mbar, u32 parity) {
   const u32 bar = smem_u32(mbar);
   asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 P, [%0], 0;\n @!P bra WAIT_%=;\n}\n" ::"r"(bar)
+      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
       : "memory");
 }
 
@@ -556,58 +547,121 @@ __device__ __forceinline__ void ld256(const u64* p, u64& a, u64& b, u64& c, u64&
   asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
 }
 
+// ---- per-tile bodies ------------------------------------------------------
+// A tile is 16 sub-transforms of one row (limb): pass A = 16 adjacent columns,
+// pass B = 16 contiguous blocks of 256.
+struct RowRef {
+  u64* ptr;
+  u32 prime;
+};
+__device__ __forceinline__ RowRef row_ref(const NttLaunch& L, u32 lane, u32 slot) {
+  return RowRef{L.base + (size_t)lane * L.lane_stride + (size_t)L.slot_off[slot] * L.n, L.prime[slot]};
+}
+
 // forward pass A: columns c = chunk*16 + lo, thread tau = hi.  canonical in, lazy out.
-__global__ void __launch_bounds__(256, 3) fwd_a(const NttLaunch L) {
-  __shared__ double sm[16 * kStride];
-  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
-  const Row r = row_of(L, row, false);
-  const double p = r.sc->pd, pinv = r.sc->pinv;
+__device__ __forceinline__ void tile_fwd_a(const NttLaunch& L, RowRef rr, u32 chunk, double* sm) {
+  const double* tw = L.tw[rr.prime].fw;
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
-  u64* col = r.ptr + chunk * 16 + lo;
-  double x[16];
+  u64* col = rr.ptr + chunk * 16 + lo;
+  double x[16], w[15];
   u64 raw[16];
 #pragma unroll
   for (int v = 0; v < 16; ++v) raw[v] = col[(size_t)(hi + 16 * v) << 8];
+  load_w<0>(w, tw, 1, 0);
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
-  ct16(x, GTw<0>{r.tw, 1, 0}, p, pinv);
+  ct16(x, WArr{w}, p, pinv);
 #pragma unroll
   for (int v = 0; v < 16; ++v) sm[lo * kStride + hi + 17 * v] = x[v];
+  load_w<4>(w, tw, 1, hi);
   __syncthreads();
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + 17 * hi + v];
-  ct16(x, GTw<4>{r.tw, 1, hi}, p, pinv);
+  ct16(x, WArr{w}, p, pinv);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
+}
+
+// fused exact conversion + forward pass A (target slot `slot` of lane `lane`):
+// the input of each element is computed from the k+1 prepared source tiles
+// (launch_conv_prep: xt_i and v in 24-bit split form) as
+// S = sum_i xt_i [B/b_i]_t + v (t - [B]_t), lazily reduced to [0, 3t).
+template <int K>
+__device__ __forceinline__ void tile_cfwd_a(const NttLaunch& L, const NttConvIn& C, u32 lane, u32 slot, u32 chunk,
+                                            double* sm) {
+  const RowRef rr = row_ref(L, lane, slot);
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
+  const ConvPlanDev* pl = C.plan;
+  const u32 m = pl->m;
+  const u64 d = pl->dst_p[slot], mu = pl->dst_mu96[slot];
+  Split hs[K + 1];
+#pragma unroll
+  for (int i = 0; i < K; ++i) hs[i] = split24(__ldg(C.hat_tab + (size_t)i * m + slot));
+  hs[K] = split24(d - pl->b_mod[slot]);
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  const size_t col0 = (size_t)chunk * 16 + lo + ((size_t)hi << 8);
+  const uint2* ps[K + 1];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    ps[i] = reinterpret_cast<const uint2*>(C.src + (size_t)lane * C.src_ls + (size_t)C.src_off[i] * (1u << 16) + col0);
+  ps[K] = reinterpret_cast<const uint2*>(C.v + (size_t)lane * C.v_ls + col0);
+  double x[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    Acc3 a;
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      const uint2 w = __ldg(ps[i] + (v << 12));
+      mac24(a, Split{w.x, w.y}, hs[i]);
+    }
+    // q = floor((S >> 32) floor(2^96/d) / 2^64) is within 3 below S/d: r = S - q d in [0, 3d)
+    const u64 top = (a.c2 << 16) + (a.c1 >> 8) + (a.c0 >> 32);
+    const u64 q = __umul64hi(top, mu);
+    const u64 s_lo = a.c0 + (a.c1 << 24) + (a.c2 << 48);
+    x[v] = u2d(s_lo - q * d);
+  }
+  double w[15];
+  load_w<0>(w, L.tw[rr.prime].fw, 1, 0);
+  ct16(x, WArr{w}, p, pinv);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sm[lo * kStride + hi + 17 * v] = x[v];
+  load_w<4>(w, L.tw[rr.prime].fw, 1, hi);
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + 17 * hi + v];
+  ct16(x, WArr{w}, p, pinv);
+  u64* col = rr.ptr + chunk * 16 + lo;
 #pragma unroll
   for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
 }
 
 // forward pass B: block b = chunk*16 + hi (256 contiguous), tau = lo.  lazy in,
 // canonical out (each thread writes its 16 contiguous outputs as 4 x 32 B).
-__global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
-  extern __shared__ double dyn[];
-  __shared__ u64 mbar;
-  double* sm = dyn;                     // 16 * kStride
-  double* stw = dyn + 16 * kStride;     // one tile blob
-  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
-  const Row r = row_of(L, row, false);
-  blob_issue(&mbar, stw, r.blob + (size_t)chunk * kNttBlobTile);
-  const double p = r.sc->pd, pinv = r.sc->pinv;
+// The caller has issued the tile's blob copy on `mbar`.
+__device__ __forceinline__ void tile_fwd_b(const NttLaunch& L, RowRef rr, u32 chunk, double* sm, const double* stw,
+                                           u64* mbar, u32 parity) {
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
-  u64* blk = r.ptr + (size_t)(chunk * 16 + hi) * 256;
-  double x[16];
+  u64* blk = rr.ptr + (size_t)(chunk * 16 + hi) * 256;
+  double x[16], w[15];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = dbits(blk[lo + 16 * v]);
-  __syncthreads();  // mbarrier initialised
-  blob_wait(&mbar);
-  const double* sb = stw + hi * kNttBlobSub;
-  ct16(x, BTw1{sb}, p, pinv);
+  load_w<0>(w, L.tw[rr.prime].fw, 256 + chunk * 16 + hi, 0);
+  ct16(x, WArr{w}, p, pinv);
   double* sp = sm + hi * kStride;
 #pragma unroll
   for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = x[v];
   __syncwarp();
+  blob_wait(mbar, parity);
+  const double* sb = stw + hi * kNttBlobSub;
+  load_w_blob(w, sb + lo);
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sp[17 * lo + v];
-  ct16(x, BTw2{sb + lo}, p, pinv);
+  ct16(x, WArr{w}, p, pinv);
   u64* o = blk + 16 * lo;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
@@ -616,69 +670,117 @@ __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
 }
 
 // inverse pass B (first): canonical in (4 x 32 B per thread), lazy out.
-__global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
-  extern __shared__ double dyn[];
-  __shared__ u64 mbar;
-  double* sm = dyn;
-  double* stw = dyn + 16 * kStride;
-  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
-  const Row r = row_of(L, row, true);
-  blob_issue(&mbar, stw, r.blob + (size_t)chunk * kNttBlobTile);
-  const double p = r.sc->pd, pinv = r.sc->pinv;
+__device__ __forceinline__ void tile_inv_b(const NttLaunch& L, RowRef rr, u32 chunk, double* sm, const double* stw,
+                                           u64* mbar, u32 parity) {
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
-  u64* blk = r.ptr + (size_t)(chunk * 16 + hi) * 256;
+  u64* blk = rr.ptr + (size_t)(chunk * 16 + hi) * 256;
   u64 raw[16];
 #pragma unroll
   for (int k = 0; k < 4; ++k) ld256(blk + 16 * lo + 4 * k, raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]);
   double x[16];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
-  __syncthreads();
-  blob_wait(&mbar);
+  double w[15];
+  blob_wait(mbar, parity);
   const double* sb = stw + hi * kNttBlobSub;
-  gs16<false>(x, BTw2{sb + lo}, p, pinv, r.sc);
+  load_w_blob(w, sb + lo);
+  gs16<false>(x, WArr{w}, p, pinv, sc);
   double* sp = sm + hi * kStride;
 #pragma unroll
   for (int v = 0; v < 16; ++v) sp[17 * lo + v] = red(x[v], p, pinv);
+  load_w<0>(w, L.tw[rr.prime].iw, 256 + chunk * 16 + hi, 0);
   __syncwarp();
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sp[lo + 17 * v];
-  gs16<false>(x, BTw1{sb}, p, pinv, r.sc);
+  gs16<false>(x, WArr{w}, p, pinv, sc);
 #pragma unroll
   for (int v = 0; v < 16; ++v) blk[lo + 16 * v] = bitsd(red(x[v], p, pinv));
 }
 
 // inverse pass A (second): columns c = chunk*16 + lo, tau = hi; lazy in, canonical out, N^{-1} folded.
-__global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
-  __shared__ double sm[16 * kStride];
-  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
-  const Row r = row_of(L, row, true);
-  const double p = r.sc->pd, pinv = r.sc->pinv;
+__device__ __forceinline__ void tile_inv_a(const NttLaunch& L, RowRef rr, u32 chunk, double* sm) {
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
-  u64* col = r.ptr + chunk * 16 + lo;
-  double x[16];
+  u64* col = rr.ptr + chunk * 16 + lo;
+  double x[16], w[15];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = dbits(col[(size_t)(16 * hi + v) << 8]);
-  gs16<false>(x, GTw<4>{r.tw, 1, hi}, p, pinv, r.sc);
+  load_w<4>(w, L.tw[rr.prime].iw, 1, hi);
+  gs16<false>(x, WArr{w}, p, pinv, sc);
 #pragma unroll
   for (int v = 0; v < 16; ++v) sm[lo * kStride + 17 * hi + v] = red(x[v], p, pinv);
+  load_w<0>(w, L.tw[rr.prime].iw, 1, 0);
   __syncthreads();
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + hi + 17 * v];
-  gs16<true>(x, GTw<0>{r.tw, 1, 0}, p, pinv, r.sc);
+  gs16<true>(x, WArr{w}, p, pinv, sc);
 #pragma unroll
   for (int v = 0; v < 16; ++v) col[(size_t)(hi + 16 * v) << 8] = canon(x[v], p, pinv);
 }
 
 constexpr size_t kSmemB = (size_t)(16 * kStride + kNttBlobTile) * sizeof(double);
 
-cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
+// ---- one-launch-per-pass kernels (slot-major rows) ---------------------------
+__device__ __forceinline__ RowRef slot_major(const NttLaunch& L, u32 row, u32& slot) {
+  slot = row / L.nlanes;
+  return row_ref(L, row - slot * L.nlanes, slot);
+}
+__global__ void __launch_bounds__(256, 3) fwd_a(const NttLaunch L) {
+  __shared__ double sm[16 * kStride];
+  u32 slot;
+  tile_fwd_a(L, slot_major(L, blockIdx.x >> 4, slot), blockIdx.x & 15, sm);
+}
+__global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
+  extern __shared__ double dyn[];
+  __shared__ u64 mbar;
+  u32 slot;
+  const RowRef rr = slot_major(L, blockIdx.x >> 4, slot);
+  const u32 chunk = blockIdx.x & 15;
+  blob_init(&mbar);
+  __syncthreads();
+  blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].fb + (size_t)chunk * kNttBlobTile);
+  tile_fwd_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
+}
+__global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
+  extern __shared__ double dyn[];
+  __shared__ u64 mbar;
+  u32 slot;
+  const RowRef rr = slot_major(L, blockIdx.x >> 4, slot);
+  const u32 chunk = blockIdx.x & 15;
+  blob_init(&mbar);
+  __syncthreads();
+  blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].ib + (size_t)chunk * kNttBlobTile);
+  tile_inv_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
+}
+__global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
+  __shared__ double sm[16 * kStride];
+  u32 slot;
+  tile_inv_a(L, slot_major(L, blockIdx.x >> 4, slot), blockIdx.x & 15, sm);
+}
+
+// fused conversion + pass A, one launch per pass: tiles ordered (lane, chunk,
+// slot fastest) so the CTAs converting one lane's column chunk run together
+template <int K>
+__global__ void __launch_bounds__(256, 3) cfwd_a(const NttLaunch L, const NttConvIn C) {
+  __shared__ double sm[16 * kStride];
+  const u32 slot = blockIdx.x % L.nslots, rest = blockIdx.x / L.nslots;
+  tile_cfwd_a<K>(L, C, rest >> 4, slot, rest & 15, sm);
+}
+
+void init_attrs() {
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(fwd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     cudaFuncSetAttribute(inv_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     init = true;
   }
+}
+
+cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
+  init_attrs();
   const u32 rows = L.nlanes * L.nslots;
   const dim3 grid(rows * 16), block(256);
   if (!inverse) {
@@ -688,6 +790,20 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
     inv_b<<<grid, block, kSmemB, st>>>(L);
     inv_a<<<grid, block, 0, st>>>(L);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, cudaStream_t st) {
+  init_attrs();
+  const dim3 grid(L.nlanes * L.nslots * 16), block(256);
+  switch (C.k) {
+    case 1: cfwd_a<1><<<grid, block, 0, st>>>(L, C); break;
+    case 2: cfwd_a<2><<<grid, block, 0, st>>>(L, C); break;
+    case 3: cfwd_a<3><<<grid, block, 0, st>>>(L, C); break;
+    case 4: cfwd_a<4><<<grid, block, 0, st>>>(L, C); break;
+    default: return cudaErrorInvalidValue;
+  }
+  fwd_b<<<grid, block, kSmemB, st>>>(L);
   return cudaGetLastError();
 }
 
@@ -722,6 +838,11 @@ void ntt_build_blob(const double* tab, double* blob) {
           d[v2::kTw1 + (1 << sg) - 1 + q] = tab[(t0 << sg) + q];
         }
     }
+}
+
+cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, cudaStream_t st) {
+  if (L.nlanes * L.nslots == 0) return cudaSuccess;
+  return v2::run_conv(L, c, st);
 }
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st) {

@@ -26,7 +26,8 @@ struct NttScale {
 // Butterfly arithmetic of the NTT passes.
 enum NttImpl : int { kNttInt = 0, kNttF64 = 1 };
 extern int g_ntt_impl;  // selected at context creation (AEGIS_NTT_IMPL=int|f64)
-extern int g_ntt_v2;    // N = 2^16 FP64 passes with direct global access (AEGIS_NTT_V2=0 disables)
+extern int g_ntt_v2;      // N = 2^16 FP64 passes with direct global access (AEGIS_NTT_V2=0 disables)
+extern int g_conv_fused;  // fused conversion + NTT (AEGIS_CONV_FUSED=0 disables)
 
 constexpr int kMaxSlots = 96;
 
@@ -48,6 +49,24 @@ constexpr int kNttBlobSub = 15 * 17 + 15;
 constexpr int kNttBlobTile = 16 * kNttBlobSub;
 // build the fwd (or inv) blob of one prime from its bit-reversed power table tab[0..2^16)
 void ntt_build_blob(const double* tab, double* blob);
+
+// Fused exact basis conversion + forward NTT (N = 2^16, k <= 4 sources): the
+// targets of L (slot s = conversion target s) are computed from the prepared
+// sources (launch_conv_prep: xt_i in place, overflow counts v) as
+//   y = sum_i xt_i [B/b_i]_t + v (t - [B]_t)  mod t
+// inside the first NTT pass, so the converted limbs never round-trip HBM.
+struct ConvPlanDev;
+struct NttConvIn {
+  const ConvPlanDev* plan;
+  const u64* hat_tab;  // [k][m] (B/b_i) mod t
+  const u64* src;      // prepared sources, coefficient domain
+  size_t src_ls;
+  u32 src_off[4];
+  u32 k;
+  const u64* v;        // overflow counts [lane][n]
+  size_t v_ls;
+};
+cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, cudaStream_t st);
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st);
 

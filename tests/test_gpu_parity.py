@@ -164,7 +164,7 @@ def test_basis_convert_random(logn, k):
         assert (got[ln, 0] == exp).all()
 
 
-@pytest.mark.parametrize("logn,level", [(4, 1), (4, 5), (10, 3), (10, 9), (12, 17), (16, 6)])
+@pytest.mark.parametrize("logn,level", [(4, 1), (4, 5), (10, 3), (10, 9), (12, 17), (16, 6), (16, 17), (16, 34)])
 @pytest.mark.parametrize("key", [0, 1007])
 def test_keyswitch(logn, level, key):
     c, o = ctx(logn), orc(logn)
@@ -180,7 +180,7 @@ def test_keyswitch(logn, level, key):
         assert (got[ln, 0] == o0).all() and (got[ln, 1] == o1).all()
 
 
-@pytest.mark.parametrize("logn,level,offset", [(10, 5, 1), (10, 17, 63), (12, 9, -1), (16, 3, 32)])
+@pytest.mark.parametrize("logn,level,offset", [(10, 5, 1), (10, 17, 63), (12, 9, -1), (16, 3, 32), (16, 17, -5)])
 def test_rot(logn, level, offset):
     c, o = ctx(logn), orc(logn)
     n = 1 << logn
@@ -229,7 +229,7 @@ def test_cmult_lane_maps():
         assert (t[ln] == o.cmult(a[2 + ln], b[ln % 2], 3)).all()
 
 
-@pytest.mark.parametrize("logn,level", [(10, 2), (10, 17), (16, 5)])
+@pytest.mark.parametrize("logn,level", [(10, 2), (10, 17), (16, 5), (16, 35)])
 def test_rescale(logn, level):
     c, o = ctx(logn), orc(logn)
     n = 1 << logn
