@@ -398,7 +398,8 @@ const u64* Context::key(u64 key_id) {
 
 // ---------------------------------------------------------------------------
 void Context::ntt(u64* base, size_t lane_stride, u32 nlanes, const std::vector<u32>& slot_off,
-                  const std::vector<u32>& primes, bool inverse) {
+                  const std::vector<u32>& primes, bool inverse, const u64* src, size_t src_ls,
+                  const std::vector<u32>* src_off) {
   if (slot_off.size() > (size_t)kMaxSlots) throw Error(AEGIS_EINVAL, "too many limbs in one NTT launch");
   NttLaunch L;
   std::memset(&L, 0, sizeof(L));
@@ -413,12 +414,18 @@ void Context::ntt(u64* base, size_t lane_stride, u32 nlanes, const std::vector<u
   }
   L.tw = d_tw;
   L.scale = d_scale;
+  if (src) {  // out-of-place inverse (v2): caller checked ntt_v2_active
+    L.in_base = src;
+    L.in_lane_stride = src_ls;
+    for (size_t i = 0; i < slot_off.size(); ++i) L.in_slot_off[i] = src_off ? (*src_off)[i] : slot_off[i];
+  }
   // grid.x holds rows * ctas_per_row; split very large batches
   const u32 max_rows = 1u << 20;
   for (u32 l0 = 0; l0 < nlanes; ) {
     u32 nl = std::max<u32>(1, std::min<u32>(nlanes - l0, max_rows / std::max<u32>(1, L.nslots)));
     NttLaunch Lb = L;
     Lb.base = base + (size_t)l0 * lane_stride;
+    if (src) Lb.in_base = src + (size_t)l0 * src_ls;
     Lb.nlanes = nl;
     AEGIS_CHECK_CUDA(ntt_run(Lb, (int)log_n, inverse, stream));
     count(2);
@@ -447,15 +454,15 @@ void Context::basis_convert(const u64* src, size_t src_ls, const std::vector<u32
 // kernel (sources -> xt in place, overflow counts -> vbuf) and the NTT whose
 // first pass computes the converted values itself (ntt.cu cfwd_a).  The
 // sources are clobbered either way (callers pass scratch limbs).
-void Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
+bool Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
                        u64* dst, size_t dst_ls, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
-                       u32 lanes, u64* vbuf) {
+                       u32 lanes, u64* vbuf, const NttFin* fin) {
   const bool fused = log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2 && g_conv_fused && src_off.size() <= 4 &&
                      dst_off.size() <= (size_t)kMaxSlots && vbuf != nullptr;
   if (!fused) {
     basis_convert(src, src_ls, src_off, src_ext, dst, dst_ls, dst_off, dst_ext, lanes);
     ntt(dst, dst_ls, lanes, dst_off, dst_ext, false);
-    return;
+    return false;
   }
   const Plan& pl = plan(src_ext, dst_ext);
   ConvIO io;
@@ -488,8 +495,9 @@ void Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off,
   c.k = pl.k;
   c.v = vbuf;
   c.v_ls = n;
-  AEGIS_CHECK_CUDA(ntt_conv_fwd(L, c, stream));
+  AEGIS_CHECK_CUDA(ntt_conv_fwd(L, c, fin, stream));
   count(2);
+  return fin != nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -520,9 +528,13 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
   u64* vbuf = dc + (size_t)B * l * n;
   for (u32 l0 = 0; l0 < lanes; l0 += B) {
     const u32 nb = std::min(B, lanes - l0);
-    AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(dc, (size_t)l * n * 8, d + (size_t)l0 * d_ls, d_ls * 8, (size_t)l * n * 8, nb,
-                                       cudaMemcpyDeviceToDevice, stream));
-    ntt(dc, (size_t)l * n, nb, main_off, main_ext, true);
+    if (ntt_v2_active((int)log_n)) {  // out-of-place INTT: d is read once, dc written once
+      ntt(dc, (size_t)l * n, nb, main_off, main_ext, true, d + (size_t)l0 * d_ls, d_ls);
+    } else {
+      AEGIS_CHECK_CUDA(cudaMemcpy2DAsync(dc, (size_t)l * n * 8, d + (size_t)l0 * d_ls, d_ls * 8, (size_t)l * n * 8, nb,
+                                         cudaMemcpyDeviceToDevice, stream));
+      ntt(dc, (size_t)l * n, nb, main_off, main_ext, true);
+    }
     for (u32 j = 0; j < S.dn; ++j) {
       const u32 lo = j * kAlpha, hi = std::min(l, lo + kAlpha);
       std::vector<u32> s_off, s_ext, t_off, t_ext;
@@ -597,8 +609,29 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
     count();
     // ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}
     ntt(acc, acc_ls, nb, p_off, p_ext, true);
-    // (lane, comp) pairs are uniform "virtual lanes" of stride ns*n / l*n
-    conv_ntt(acc, (size_t)ns * n, ps_off, ps_ext, pcv, (size_t)l * n, main_off, main_ext, 2 * nb, vbuf);
+    // (lane, comp) pairs are uniform "virtual lanes" of stride ns*n / l*n;
+    // the finish (acc_Q - conv) * P^{-1} + add (+ automorphism) is fused into
+    // the last NTT pass when available
+    NttFin fin;
+    std::memset(&fin, 0, sizeof(fin));
+    fin.x = acc;
+    fin.x_lane = (long long)acc_ls;
+    fin.x_comp = (long long)ns * n;
+    fin.add = o.add[0] ? o.add[0] + (size_t)l0 * o.add_lane[0] : nullptr;
+    fin.add_lane = (long long)o.add_lane[0];
+    fin.add_comp = o.add[1] ? (long long)(o.add[1] - o.add[0]) : 0;
+    fin.add_comps = o.add[1] ? 2 : 1;
+    fin.out = o.out[0] + (size_t)l0 * o.out_lane[0];
+    fin.out_lane = (long long)o.out_lane[0];
+    fin.out_comp = (long long)(o.out[1] - o.out[0]);
+    fin.comps = 2;
+    fin.galois_inv = galois <= 1 ? 1 : h_powmod(galois, (u64)n - 1, 2ull * n);
+    fin.log_n = log_n;
+    for (u32 i = 0; i < l; ++i) fin.f[i] = f.f[i];
+    const bool uniform = o.out_lane[0] == o.out_lane[1] && (!o.add[1] || o.add_lane[0] == o.add_lane[1]);
+    if (conv_ntt(acc, (size_t)ns * n, ps_off, ps_ext, pcv, (size_t)l * n, main_off, main_ext, 2 * nb, vbuf,
+                 uniform ? &fin : nullptr))
+      continue;  // finished inside the NTT
     for (u32 c = 0; c < 2; ++c) {
       f.x = acc + (size_t)c * ns * n;
       f.x_lane = acc_ls;
@@ -722,14 +755,33 @@ void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im
   for (u32 l0 = 0; l0 < lanes; l0 += B) {
     const u32 nb = std::min(B, lanes - l0);
     // last limb of every (lane, comp) -> [lane][comp][n], Intt, centred lift to q_0..q_{L-2}, Ntt
-    AEGIS_CHECK_CUDA(launch_copy(View{last, nb, 2, 1}, 0, in.view(), LaneMap{im.lane0 + l0, nb}, nb, 2, 1, L - 1, n,
-                                 stream));
-    count();
-    ntt(last, n, 2 * nb, {0}, {L - 1}, true);
-    conv_ntt(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * nb, vbuf);
-    // out_i = (x_i - r_i) * q_{L-1}^{-1}   (div_round on the centred value, rns_math.hpp:196-202)
+    const bool v2 = ntt_v2_active((int)log_n) && in.comps == 2;
+    if (v2) {  // (lane, comp) are uniform virtual lanes of stride level*n when comps == 2
+      const std::vector<u32> src_off{L - 1};
+      ntt(last, n, 2 * nb, {0}, {L - 1}, true, in.view().limb(im.lane0 + l0, 0, 0, n), (size_t)in.level * n, &src_off);
+    } else {
+      AEGIS_CHECK_CUDA(launch_copy(View{last, nb, 2, 1}, 0, in.view(), LaneMap{im.lane0 + l0, nb}, nb, 2, 1, L - 1, n,
+                                   stream));
+      count();
+      ntt(last, n, 2 * nb, {0}, {L - 1}, true);
+    }
+    // out_i = (x_i - r_i) * q_{L-1}^{-1}   (div_round on the centred value, rns_math.hpp:196-202),
+    // fused into the conversion NTT's last pass when available
     f.x = in.view().limb(im.lane0 + l0, 0, 0, n);
     f.out = out.view().limb(out_lane + l0, 0, 0, n);
+    NttFin fin;
+    std::memset(&fin, 0, sizeof(fin));
+    fin.x = f.x;
+    fin.x_lane = (long long)f.x_lane;
+    fin.x_comp = (long long)f.x_comp;
+    fin.out = f.out;
+    fin.out_lane = (long long)f.out_lane;
+    fin.out_comp = (long long)f.out_comp;
+    fin.comps = 2;
+    fin.galois_inv = 1;
+    fin.log_n = log_n;
+    for (u32 i = 0; i < m; ++i) fin.f[i] = f.f[i];
+    if (conv_ntt(last, n, {0}, {L - 1}, conv, (size_t)m * n, off, ext, 2 * nb, vbuf, &fin)) continue;
     AEGIS_CHECK_CUDA(launch_finish(f, nb, n, d_pc, stream));
     count();
   }

@@ -85,16 +85,21 @@ class Context {
 
   // ---- polynomial instructions --------------------------------------------
   // NTT over rows: lanes x slots, slot_off[i] limbs into the lane, primes[i]
+  // src (inverse, v2 only): read the input from src + lane*src_ls + src_off[slot]*n
+  // (src_off defaults to slot_off) and write the result to base
   void ntt(u64* base, size_t lane_stride, u32 nlanes, const std::vector<u32>& slot_off,
-           const std::vector<u32>& primes, bool inverse);
+           const std::vector<u32>& primes, bool inverse, const u64* src = nullptr, size_t src_ls = 0,
+           const std::vector<u32>* src_off = nullptr);
   void basis_convert(const u64* src, size_t src_lane_stride, const std::vector<u32>& src_off,
                      const std::vector<u32>& src_ext, u64* dst, size_t dst_lane_stride,
                      const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext, u32 lanes);
   // exact conversion + forward NTT of the targets (fused at N = 2^16, k <= 4);
-  // clobbers the sources; vbuf: lanes * n words of scratch
-  void conv_ntt(u64* src, size_t src_lane_stride, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
+  // clobbers the sources; vbuf: lanes * n words of scratch.  With `fin` the
+  // finish epilogue is fused into the last pass when the fused path runs
+  // (returns true); otherwise dst holds the NTT and the caller finishes.
+  bool conv_ntt(u64* src, size_t src_lane_stride, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
                 u64* dst, size_t dst_lane_stride, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
-                u32 lanes, u64* vbuf);
+                u32 lanes, u64* vbuf, const NttFin* fin = nullptr);
   // Hybrid key switch (poly_ir.hpp:219-298) of `lanes` polynomials d (level
   // limbs each, NTT domain, lane stride d_ls).  out_c = add_c + KS_c(d).
   struct KsOut {

@@ -669,16 +669,75 @@ __device__ __forceinline__ void tile_fwd_b(const NttLaunch& L, RowRef rr, u32 ch
           canon(x[4 * k + 3], p, pinv));
 }
 
-// inverse pass B (first): canonical in (4 x 32 B per thread), lazy out.
-__device__ __forceinline__ void tile_inv_b(const NttLaunch& L, RowRef rr, u32 chunk, double* sm, const double* stw,
-                                           u64* mbar, u32 parity) {
+// forward pass B with the ModDown / rescale finish epilogue (see NttFin)
+__device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin& F, u32 lane_v, u32 slot, u32 chunk,
+                                               double* sm, const double* stw, u64* mbar, u32 parity) {
+  const RowRef rr = row_ref(L, lane_v, slot);
   const NttScale* sc = L.scale + rr.prime;
   const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
   u64* blk = rr.ptr + (size_t)(chunk * 16 + hi) * 256;
+  double x[16], w[15];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = dbits(blk[lo + 16 * v]);
+  load_w<0>(w, L.tw[rr.prime].fw, 256 + chunk * 16 + hi, 0);
+  ct16(x, WArr{w}, p, pinv);
+  double* sp = sm + hi * kStride;
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = x[v];
+  __syncwarp();
+  blob_wait(mbar, parity);
+  load_w_blob(w, stw + hi * kNttBlobSub + lo);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[17 * lo + v];
+  ct16(x, WArr{w}, p, pinv);
+  // epilogue
+  const u32 lane = lane_v / F.comps, comp = lane_v - lane * F.comps;
+  const size_t s0 = (size_t)(chunk * 16 + hi) * 256 + 16 * lo;  // first of this thread's 16 positions
+  const u64* xr = F.x + (long long)lane * F.x_lane + (long long)comp * F.x_comp + (size_t)slot * L.n + s0;
+  const double f = u2d(F.f[slot]), fp = f * pinv;
+  u64 xv[16];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ld256(xr + 4 * k, xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = mm(u2d(xv[v]) - x[v], f, fp, p);
+  if (F.add && comp < F.add_comps) {
+    const u64* ar = F.add + (long long)lane * F.add_lane + (long long)comp * F.add_comp + (size_t)slot * L.n + s0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ld256(ar + 4 * k, xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] += u2d(xv[v]);
+  }
+  u64* orow = F.out + (long long)lane * F.out_lane + (long long)comp * F.out_comp + (size_t)slot * L.n;
+  if (F.galois_inv <= 1) {
+    u64* o = orow + s0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      st256(o + 4 * k, canon(x[4 * k], p, pinv), canon(x[4 * k + 1], p, pinv), canon(x[4 * k + 2], p, pinv),
+            canon(x[4 * k + 3], p, pinv));
+  } else {
+    // out[pi^-1(s)] = z[s]: eval-domain automorphism applied as a scatter
+    const u32 mask = 2u * L.n - 1, k = (u32)(F.galois_inv & mask), sh = 32 - F.log_n;
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      const u32 s = (u32)s0 + v;
+      const u32 t = __brev(((((__brev(s) >> sh) * 2 + 1) * k & mask) - 1) >> 1) >> sh;
+      orow[t] = canon(x[v], p, pinv);
+    }
+  }
+}
+
+// inverse pass B (first): canonical in (4 x 32 B per thread), lazy out.
+__device__ __forceinline__ void tile_inv_b(const NttLaunch& L, RowRef rr, const u64* src_row, u32 chunk, double* sm,
+                                           const double* stw, u64* mbar, u32 parity) {
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  u64* blk = rr.ptr + (size_t)(chunk * 16 + hi) * 256;
+  const u64* sblk = src_row + (size_t)(chunk * 16 + hi) * 256;
   u64 raw[16];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) ld256(blk + 16 * lo + 4 * k, raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]);
+  for (int k = 0; k < 4; ++k) ld256(sblk + 16 * lo + 4 * k, raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]);
   double x[16];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
@@ -744,16 +803,30 @@ __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].fb + (size_t)chunk * kNttBlobTile);
   tile_fwd_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
+__global__ void __launch_bounds__(256, 3) fwd_b_fin(const NttLaunch L, const NttFin F) {
+  extern __shared__ double dyn[];
+  __shared__ u64 mbar;
+  const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
+  const u32 slot = row / L.nlanes, lane_v = row - slot * L.nlanes;
+  blob_init(&mbar);
+  __syncthreads();
+  blob_issue(&mbar, dyn + 16 * kStride, L.tw[L.prime[slot]].fb + (size_t)chunk * kNttBlobTile);
+  tile_fwd_b_fin(L, F, lane_v, slot, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
+}
 __global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
   extern __shared__ double dyn[];
   __shared__ u64 mbar;
   u32 slot;
-  const RowRef rr = slot_major(L, blockIdx.x >> 4, slot);
+  const u32 row = blockIdx.x >> 4;
+  const RowRef rr = slot_major(L, row, slot);
   const u32 chunk = blockIdx.x & 15;
+  const u64* src = L.in_base ? L.in_base + (size_t)(row - slot * L.nlanes) * L.in_lane_stride +
+                                   (size_t)L.in_slot_off[slot] * L.n
+                             : rr.ptr;
   blob_init(&mbar);
   __syncthreads();
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].ib + (size_t)chunk * kNttBlobTile);
-  tile_inv_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
+  tile_inv_b(L, rr, src, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
 __global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
   __shared__ double sm[16 * kStride];
@@ -775,6 +848,7 @@ void init_attrs() {
   if (!init) {
     cudaFuncSetAttribute(fwd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     cudaFuncSetAttribute(inv_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
+    cudaFuncSetAttribute(fwd_b_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     init = true;
   }
 }
@@ -793,7 +867,7 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, cudaStream_t st) {
+cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, cudaStream_t st) {
   init_attrs();
   const dim3 grid(L.nlanes * L.nslots * 16), block(256);
   switch (C.k) {
@@ -803,7 +877,16 @@ cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, cudaStream_t st) {
     case 4: cfwd_a<4><<<grid, block, 0, st>>>(L, C); break;
     default: return cudaErrorInvalidValue;
   }
-  fwd_b<<<grid, block, kSmemB, st>>>(L);
+  if (fin) fwd_b_fin<<<grid, block, kSmemB, st>>>(L, *fin);
+  else fwd_b<<<grid, block, kSmemB, st>>>(L);
+  return cudaGetLastError();
+}
+
+cudaError_t run_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) {
+  init_attrs();
+  const dim3 grid(L.nlanes * L.nslots * 16), block(256);
+  fwd_a<<<grid, block, 0, st>>>(L);
+  fwd_b_fin<<<grid, block, kSmemB, st>>>(L, fin);
   return cudaGetLastError();
 }
 
@@ -840,13 +923,20 @@ void ntt_build_blob(const double* tab, double* blob) {
     }
 }
 
-cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, cudaStream_t st) {
+cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, const NttFin* fin, cudaStream_t st) {
   if (L.nlanes * L.nslots == 0) return cudaSuccess;
-  return v2::run_conv(L, c, st);
+  return v2::run_conv(L, c, fin, st);
 }
+cudaError_t ntt_fwd_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) {
+  if (L.nlanes * L.nslots == 0) return cudaSuccess;
+  return v2::run_fin(L, fin, st);
+}
+
+bool ntt_v2_active(int log_n) { return log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2; }
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st) {
   if (L.nlanes * L.nslots == 0) return cudaSuccess;
+  if (L.in_base && !(inverse && ntt_v2_active(log_n))) return cudaErrorInvalidValue;
   if (log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2) return v2::run(L, inverse, st);
   return g_ntt_impl == kNttF64 ? run_impl<kNttF64>(L, log_n, inverse, st) : run_impl<kNttInt>(L, log_n, inverse, st);
 }

@@ -41,6 +41,11 @@ struct NttLaunch {
   unsigned char prime[kMaxSlots];
   const PrimeTw* tw;       // device, indexed by ext prime
   const NttScale* scale;   // device, indexed by ext prime
+  // optional out-of-place input of the first inverse pass (v2 only):
+  // row (lane, slot) reads in_base + lane*in_lane_stride + in_slot_off[slot]*n
+  const u64* in_base;
+  size_t in_lane_stride;
+  u32 in_slot_off[kMaxSlots];
 };
 
 // pass-B twiddle blob of one 16-sub tile at N = 2^16 (ntt.cu v2):
@@ -66,7 +71,26 @@ struct NttConvIn {
   const u64* v;        // overflow counts [lane][n]
   size_t v_ls;
 };
-cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, cudaStream_t st);
+// Optional epilogue of the second forward pass (ModDown / rescale finish):
+// for virtual lane vl = lane * comps + comp and slot i of the launch,
+//   z[s]  = (x[s] - y[s]) * f_i  (+ add[s] when comp < add_comps)
+//   out[t] = z[s] at t = s (galois_inv <= 1) or t = pi_{galois_inv}(s)
+// where y is the NTT output; y itself is never written to HBM.
+struct NttFin {
+  const u64* x;  long long x_lane, x_comp;
+  const u64* add; long long add_lane, add_comp;
+  u64* out; long long out_lane, out_comp;
+  u32 comps, add_comps;
+  u64 galois_inv;
+  u32 log_n;
+  u64 f[kMaxSlots];
+};
+cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, const NttFin* fin, cudaStream_t st);
+// plain forward NTT with the finish epilogue (sources already converted)
+cudaError_t ntt_fwd_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st);
+
+// true when ntt_run uses the v2 passes (out-of-place inverse, fused epilogues available)
+bool ntt_v2_active(int log_n);
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st);
 
