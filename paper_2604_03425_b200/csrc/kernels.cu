@@ -298,6 +298,45 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
   }
 }
 
+// Key product with every load of a coefficient issued up front: DN ext/d
+// words and 2*DN key words per thread are in flight together (the looped
+// form exposes one memory latency per digit).  Lanes vary fastest across the
+// grid so CTAs in flight share the key tile of one (slot, chunk) in L2.
+template <int DN>
+__global__ void __launch_bounds__(256) keymul_dn_kernel(const KeyMulIO io, u32 lanes, u32 n,
+                                                        const PrimeConst* __restrict__ pc) {
+  const u32 chunks = n / 256;
+  const u32 lane = blockIdx.x % lanes, rest = blockIdx.x / lanes;
+  const u32 chunk = rest % chunks, slot = rest / chunks;
+  const u32 x = chunk * 256 + threadIdx.x;
+  const PrimeConst P = pc[io.slot_ext[slot]];
+  const size_t kslot_stride = (size_t)io.key_slots * n;
+  const u64* kb = io.key + (size_t)io.slot_key[slot] * n + x;
+  const u64* eb = io.ext + (size_t)lane * io.ext_lane_stride + x;
+  const u64* db = io.d + (size_t)lane * io.d_lane_stride + (size_t)slot * n + x;
+  const bool main_slot = slot < io.level;
+  u64 e[DN], k0[DN], k1[DN];
+#pragma unroll
+  for (int j = 0; j < DN; ++j) {
+    const u32 lo = j * kAlpha, hi = lo + kAlpha < io.level ? lo + kAlpha : io.level;
+    const bool own = main_slot && slot >= lo && slot < hi;
+    const u32 idx = j * io.nslots - lo + (slot < lo ? slot : slot - (hi - lo));
+    e[j] = own ? db[0] : eb[(size_t)idx * n];
+    k0[j] = __ldg(kb + (size_t)j * 2 * kslot_stride);
+    k1[j] = __ldg(kb + (size_t)j * 2 * kslot_stride + kslot_stride);
+  }
+  Acc3 s0, s1;
+#pragma unroll
+  for (int j = 0; j < DN; ++j) {
+    const Split v = split24(e[j]);
+    mac24(s0, v, split24(k0[j]));
+    mac24(s1, v, split24(k1[j]));
+  }
+  u64* a0 = io.acc + (size_t)lane * io.acc_lane_stride + (size_t)slot * n + x;
+  a0[0] = acc3_reduce(s0, P.p, P.mu104);
+  a0[(size_t)io.nslots * n] = acc3_reduce(s1, P.p, P.mu104);
+}
+
 __global__ void finish_kernel(const FinishIO io, u32 n, const PrimeConst* __restrict__ pc, u32 cpr) {
   const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
   const u32 lb = row % io.limbs, rest = row / io.limbs, comp = rest % io.comps, lane = rest / io.comps;
@@ -500,6 +539,16 @@ cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, con
 }
 
 cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  if (n >= 256 && io.dnum >= 1 && io.dnum <= 9) {
+    const size_t g = (size_t)lanes * io.nslots * (n / 256);
+#define AEGIS_KM(D) \
+  case D: keymul_dn_kernel<D><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+    switch (io.dnum) {
+      AEGIS_KM(1) AEGIS_KM(2) AEGIS_KM(3) AEGIS_KM(4) AEGIS_KM(5) AEGIS_KM(6) AEGIS_KM(7) AEGIS_KM(8) AEGIS_KM(9)
+    }
+#undef AEGIS_KM
+    return cudaGetLastError();
+  }
   const u32 cpr = chunks_of(n);
   const size_t g = (size_t)lanes * io.nslots * cpr;
   if (!g) return cudaSuccess;
