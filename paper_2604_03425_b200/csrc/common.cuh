@@ -145,6 +145,27 @@ __device__ __forceinline__ u128 acc3_value(const Acc3& s) {
 // sum < 2^104 (<= 256 products of 48-bit residues) -> canonical residue
 __device__ __forceinline__ u64 acc3_reduce(const Acc3& s, u64 p, u64 mu) { return reduce104(acc3_value(s), p, mu); }
 
+// ---- exact FP64 modular arithmetic (p < 2^46; see ntt.cu v2 for the bounds) ----
+constexpr double kF64Magic = 6755399441055744.0;  // 1.5 * 2^52: round on the DFMA pipe
+constexpr double kF64Two52 = 4503599627370496.0;
+__device__ __forceinline__ double f64_of(u64 x) {  // exact for x < 2^52
+  return __longlong_as_double((long long)(x | 0x4330000000000000ULL)) - kF64Two52;
+}
+// y * w mod p in [-1.5p, 1.5p] for |y * w / p| < 2^51, wp ~ w / p
+__device__ __forceinline__ double f64_mulmod(double y, double w, double wp, double p) {
+  const double h = y * w;
+  const double l = fma(y, w, -h);
+  const double q = fma(y, wp, kF64Magic) - kF64Magic;
+  return fma(-q, p, h) + l;
+}
+// |x| < 2^51 -> canonical residue
+__device__ __forceinline__ u64 f64_canon(double x, double p, double pinv) {
+  double r = fma(-((x * pinv + kF64Magic) - kF64Magic), p, x);
+  r = r < 0.0 ? r + p : r;
+  r = r >= p ? r - p : r;
+  return (u64)__double_as_longlong(r + kF64Two52) & 0xFFFFFFFFFFFFFULL;
+}
+
 #endif  // __CUDACC__
 
 }  // namespace aegis

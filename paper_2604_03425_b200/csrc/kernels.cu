@@ -302,7 +302,7 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
 // words and 2*DN key words per thread are in flight together (the looped
 // form exposes one memory latency per digit).  Lanes vary fastest across the
 // grid so CTAs in flight share the key tile of one (slot, chunk) in L2.
-template <int DN>
+template <int DN, bool F64>
 __global__ void __launch_bounds__(256) keymul_dn_kernel(const KeyMulIO io, u32 lanes, u32 n,
                                                         const PrimeConst* __restrict__ pc) {
   const u32 chunks = n / 256;
@@ -325,16 +325,31 @@ __global__ void __launch_bounds__(256) keymul_dn_kernel(const KeyMulIO io, u32 l
     k0[j] = __ldg(kb + (size_t)j * 2 * kslot_stride);
     k1[j] = __ldg(kb + (size_t)j * 2 * kslot_stride + kslot_stride);
   }
-  Acc3 s0, s1;
+  u64* a0 = io.acc + (size_t)lane * io.acc_lane_stride + (size_t)slot * n + x;
+  if constexpr (!F64) {
+    Acc3 s0, s1;
+#pragma unroll
+    for (int j = 0; j < DN; ++j) {
+      const Split v = split24(e[j]);
+      mac24(s0, v, split24(k0[j]));
+      mac24(s1, v, split24(k1[j]));
+    }
+    a0[0] = acc3_reduce(s0, P.p, P.mu104);
+    a0[(size_t)io.nslots * n] = acc3_reduce(s1, P.p, P.mu104);
+    return;
+  }
+  // exact FP64 products on the otherwise idle DFMA pipe (the 24-bit integer
+  // MACs make this kernel ALU-bound); DN terms in [-1.5p, 1.5p] sum exactly
+  const double pd = f64_of(P.p), pinv = 1.0 / pd;
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int j = 0; j < DN; ++j) {
-    const Split v = split24(e[j]);
-    mac24(s0, v, split24(k0[j]));
-    mac24(s1, v, split24(k1[j]));
+    const double v = f64_of(e[j]), w0 = f64_of(k0[j]), w1 = f64_of(k1[j]);
+    s0 += f64_mulmod(v, w0, w0 * pinv, pd);
+    s1 += f64_mulmod(v, w1, w1 * pinv, pd);
   }
-  u64* a0 = io.acc + (size_t)lane * io.acc_lane_stride + (size_t)slot * n + x;
-  a0[0] = acc3_reduce(s0, P.p, P.mu104);
-  a0[(size_t)io.nslots * n] = acc3_reduce(s1, P.p, P.mu104);
+  a0[0] = f64_canon(s0, pd, pinv);
+  a0[(size_t)io.nslots * n] = f64_canon(s1, pd, pinv);
 }
 
 __global__ void finish_kernel(const FinishIO io, u32 n, const PrimeConst* __restrict__ pc, u32 cpr) {
@@ -418,6 +433,8 @@ __global__ void weight_rowkeys_kernel(u64* out, u32 wlanes, u32 limbs, u64 seed,
 }
 
 }  // namespace
+
+int g_km_f64 = 1;
 
 // ---------------------------------------------------------------------------
 // launch wrappers
@@ -542,7 +559,10 @@ cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst
   if (n >= 256 && io.dnum >= 1 && io.dnum <= 9) {
     const size_t g = (size_t)lanes * io.nslots * (n / 256);
 #define AEGIS_KM(D) \
-  case D: keymul_dn_kernel<D><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+  case D:                                                                                       \
+    if (g_km_f64) keymul_dn_kernel<D, true><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc);      \
+    else keymul_dn_kernel<D, false><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc);              \
+    break;
     switch (io.dnum) {
       AEGIS_KM(1) AEGIS_KM(2) AEGIS_KM(3) AEGIS_KM(4) AEGIS_KM(5) AEGIS_KM(6) AEGIS_KM(7) AEGIS_KM(8) AEGIS_KM(9)
     }

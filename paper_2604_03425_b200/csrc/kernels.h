@@ -108,6 +108,7 @@ struct KeyMulIO {
   u32 slot_ext[kMaxConv + 8];  // ext prime of slot
   u32 slot_key[kMaxConv + 8];  // key slot of slot
 };
+extern int g_km_f64;  // key product on the DFMA pipe (AEGIS_KM_F64=0: 24-bit integer MACs)
 cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst* pc, cudaStream_t st);
 
 // ModDown / rescale finish: out_c[i] = add_c[i] + (x_c[i] - y_c[i]) * f_i mod q_i
