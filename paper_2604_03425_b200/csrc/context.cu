@@ -626,6 +626,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
     fin.out_lane = (long long)o.out_lane[0];
     fin.out_comp = (long long)(o.out[1] - o.out[0]);
     fin.comps = 2;
+    fin.galois = galois;
     fin.galois_inv = galois <= 1 ? 1 : h_powmod(galois, (u64)n - 1, 2ull * n);
     fin.log_n = log_n;
     for (u32 i = 0; i < l; ++i) fin.f[i] = f.f[i];

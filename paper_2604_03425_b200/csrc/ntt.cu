@@ -693,37 +693,59 @@ __device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin&
   ct16(x, WArr{w}, p, pinv);
   // epilogue
   const u32 lane = lane_v / F.comps, comp = lane_v - lane * F.comps;
-  const size_t s0 = (size_t)(chunk * 16 + hi) * 256 + 16 * lo;  // first of this thread's 16 positions
-  const u64* xr = F.x + (long long)lane * F.x_lane + (long long)comp * F.x_comp + (size_t)slot * L.n + s0;
+  const u32 sl = (hi << 8) + 16 * lo;                   // this thread's first position inside the tile
+  const size_t s0 = (size_t)chunk * 4096 + sl;          // ... inside the limb
   const double f = u2d(F.f[slot]), fp = f * pinv;
-  u64 xv[16];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ld256(xr + 4 * k, xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
-#pragma unroll
-  for (int v = 0; v < 16; ++v) x[v] = mm(u2d(xv[v]) - x[v], f, fp, p);
-  if (F.add && comp < F.add_comps) {
-    const u64* ar = F.add + (long long)lane * F.add_lane + (long long)comp * F.add_comp + (size_t)slot * L.n + s0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ld256(ar + 4 * k, xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
-#pragma unroll
-    for (int v = 0; v < 16; ++v) x[v] += u2d(xv[v]);
-  }
+  const bool has_add = F.add && comp < F.add_comps;
+  const u64* xr = F.x + (long long)lane * F.x_lane + (long long)comp * F.x_comp + (size_t)slot * L.n + s0;
+  const u64* ar = has_add ? F.add + (long long)lane * F.add_lane + (long long)comp * F.add_comp + (size_t)slot * L.n + s0
+                          : nullptr;
   u64* orow = F.out + (long long)lane * F.out_lane + (long long)comp * F.out_comp + (size_t)slot * L.n;
-  if (F.galois_inv <= 1) {
-    u64* o = orow + s0;
+  const bool permute = F.galois_inv > 1;
+  u64* su = reinterpret_cast<u64*>(sm);  // permuted output staging: 4096 words of the tile
+  if (permute) __syncthreads();          // every thread is done with the exchange rows
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      st256(o + 4 * k, canon(x[4 * k], p, pinv), canon(x[4 * k + 1], p, pinv), canon(x[4 * k + 2], p, pinv),
-            canon(x[4 * k + 3], p, pinv));
-  } else {
-    // out[pi^-1(s)] = z[s]: eval-domain automorphism applied as a scatter
-    const u32 mask = 2u * L.n - 1, k = (u32)(F.galois_inv & mask), sh = 32 - F.log_n;
+  for (int k = 0; k < 4; ++k) {  // 4 positions at a time keeps the live state small
+    u64 xv[4];
+    ld256(xr + 4 * k, xv[0], xv[1], xv[2], xv[3]);
+    double z[4];
 #pragma unroll
-    for (int v = 0; v < 16; ++v) {
-      const u32 s = (u32)s0 + v;
-      const u32 t = __brev(((((__brev(s) >> sh) * 2 + 1) * k & mask) - 1) >> 1) >> sh;
-      orow[t] = canon(x[v], p, pinv);
+    for (int i = 0; i < 4; ++i) z[i] = mm(u2d(xv[i]) - x[4 * k + i], f, fp, p);
+    if (has_add) {
+      ld256(ar + 4 * k, xv[0], xv[1], xv[2], xv[3]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) z[i] += u2d(xv[i]);
     }
+    const u64 c0 = canon(z[0], p, pinv), c1 = canon(z[1], p, pinv), c2 = canon(z[2], p, pinv),
+              c3 = canon(z[3], p, pinv);
+    if (!permute) {
+      st256(orow + s0 + 4 * k, c0, c1, c2, c3);
+    } else {
+      su[sl + 4 * k] = c0;
+      su[sl + 4 * k + 1] = c1;
+      su[sl + 4 * k + 2] = c2;
+      su[sl + 4 * k + 3] = c3;
+    }
+  }
+  if (permute) {
+    // out[t] = z[pi(t)]: pi maps aligned 32-blocks onto aligned 32-blocks, so
+    // the tile's 128 source blocks are 128 whole target blocks; each thread
+    // gathers half a target block from SMEM and writes it with 256-bit stores.
+    __syncthreads();
+    const u32 mask = 2u * L.n - 1, sh = 32 - F.log_n;
+    const u32 kf = (u32)(F.galois & mask), ki = (u32)(F.galois_inv & mask);
+    const u32 sb = (u32)chunk * 4096 + (threadIdx.x >> 1) * 32;  // source block of this thread pair
+    const u32 tb = (__brev(((((__brev(sb) >> sh) * 2 + 1) * ki & mask) - 1) >> 1) >> sh) & ~31u;
+    const u32 t0 = tb + 16 * (threadIdx.x & 1);
+    u64 w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const u32 t = t0 + i;
+      const u32 sidx = __brev(((((__brev(t) >> sh) * 2 + 1) * kf & mask) - 1) >> 1) >> sh;
+      w[i] = su[sidx - (u32)chunk * 4096];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st256(orow + t0 + 4 * k, w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
   }
 }
 

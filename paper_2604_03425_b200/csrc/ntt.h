@@ -81,7 +81,7 @@ struct NttFin {
   const u64* add; long long add_lane, add_comp;
   u64* out; long long out_lane, out_comp;
   u32 comps, add_comps;
-  u64 galois_inv;
+  u64 galois, galois_inv;  // galois_inv <= 1: no automorphism
   u32 log_n;
   u64 f[kMaxSlots];
 };
