@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace aegis {
 
@@ -100,6 +103,9 @@ bool Arena::grow(size_t need) {
       return false;
     }
     chunks_.push_back(Chunk{mapped_, sz, h});
+    if (std::getenv("AEGIS_DEBUG"))
+      fprintf(stderr, "[aegis] arena grow +%zu MiB -> %zu MiB mapped (request %zu MiB)\n", sz >> 20, (mapped_ + sz) >> 20,
+              need >> 20);
     // new space joins the free block at the tail, if any
     size_t off = mapped_, len = sz;
     if (!free_.empty()) {

@@ -112,7 +112,8 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.reduce_user = g->reduce_user;
   opt.hoist = g->hoist != 0;
   if (g->profile) opt.op_ms = &g->op_ms;
-  c.trim();
+  // no trim here: the arena keeps its mapping across runs (re-mapping ~130 GB
+  // per layer run stalled the stream); key allocation trims on demand
   c.peak_bytes = c.live_bytes;
   aegis::Executor ex(c, g->g, opt);
   ex.run();

@@ -357,6 +357,11 @@ void Context::generate_key(u64 key_id) {
   u64* k = nullptr;
   const size_t words = (size_t)key_digits() * 2 * key_slots() * n;
   cudaError_t e = cudaMalloc(&k, words * 8);
+  if (e != cudaSuccess) {  // idle arena / pool memory may hold the space: release it and retry
+    cudaGetLastError();
+    trim();
+    e = cudaMalloc(&k, words * 8);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error(AEGIS_EOOM, "key allocation failed");

@@ -12,6 +12,7 @@ import argparse
 import os
 import sys
 import tempfile
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -66,13 +67,18 @@ def main():
             g.run()
             g.run()
             ts = []
+            hs = []
             for _ in range(a.reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
+                h0 = time.perf_counter()
                 g.run()
+                hs.append(round((time.perf_counter() - h0) * 1e3, 1))
                 e1.record(st)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
+            if os.environ.get("AEGIS_DEBUG"):
+                print("  host ms per run (enqueue):", hs)
             ms = min(ts)
             units = a.lanes * (a.rots if w == "rot" else 1)
             print(f"{w:8s} {a.lanes} lanes: {ms:9.3f} ms/run  {ms * 1e3 / units:8.1f} us per lane-op "
