@@ -328,7 +328,7 @@ def ntt_roofline(c, st):
         traffic = json.load(open(os.path.join(ROOT, "profiles", "ntt_traffic.json")))["bytes_per_launch"]
     except Exception:
         pass
-    return {"kernel": "ntt_pass_kernel (fwd, 2 passes, 816 limbs of N=2^16)", "bound": "hbm",
+    return {"kernel": "NTT v2 fwd_a + fwd_b (forward, 2 passes, 816 limbs of N=2^16)", "bound": "hbm",
             "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
             "frac": achieved / pk.get("hbm_gbs"), "traffic": traffic,
             "peak_source": "measured" if not pk.get("_fallback") else "fallback",
