@@ -145,6 +145,14 @@ __device__ __forceinline__ u128 acc3_value(const Acc3& s) {
 // sum < 2^104 (<= 256 products of 48-bit residues) -> canonical residue
 __device__ __forceinline__ u64 acc3_reduce(const Acc3& s, u64 p, u64 mu) { return reduce104(acc3_value(s), p, mu); }
 
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256), 32-byte aligned
+__device__ __forceinline__ void ld256g(const u64* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+__device__ __forceinline__ void st256g(u64* p, u64 a, u64 b, u64 c, u64 d) {
+  asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
 // ---- exact FP64 modular arithmetic (p < 2^46; see ntt.cu v2 for the bounds) ----
 constexpr double kF64Magic = 6755399441055744.0;  // 1.5 * 2^52: round on the DFMA pipe
 constexpr double kF64Two52 = 4503599627370496.0;

@@ -91,22 +91,22 @@ __global__ void cmult_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b
   }
 }
 
-__global__ void cadd_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, int acc,
-                            u32 nlanes, u32 comps, u32 limbs, u32 n, const PrimeConst* __restrict__ pc,
-                            u32 cpr) {
+// 4 contiguous coefficients per thread with 256-bit accesses (HBM-bound)
+__global__ void __launch_bounds__(256) cadd_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb,
+                                                   int acc, u32 nlanes, u32 comps, u32 limbs, u32 n,
+                                                   const PrimeConst* __restrict__ pc, u32 cpr) {
   const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
   const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, l = rest / comps;
   const u64 p = pc[lb].p;
-  const u64* x = a.limb(ma.at(l, nlanes), comp, lb, n);
-  u64* d = out.limb(out_lane0 + l, comp, lb, n);
-  if (acc) {
-    for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
-      d[t] = add_mod(d[t], x[t], p);
-  } else {
-    const u64* y = b.limb(mb.at(l, nlanes), comp, lb, n);
-    for (u32 t = chunk * kChunk + threadIdx.x; t < n && t < (chunk + 1) * kChunk; t += kThreads)
-      d[t] = add_mod(x[t], y[t], p);
-  }
+  const u32 t = (chunk * 256 + threadIdx.x) * 4;
+  if (t >= n) return;
+  const u64* x = a.limb(ma.at(l, nlanes), comp, lb, n) + t;
+  u64* d = out.limb(out_lane0 + l, comp, lb, n) + t;
+  const u64* y = acc ? d : b.limb(mb.at(l, nlanes), comp, lb, n) + t;
+  u64 x0, x1, x2, x3, y0, y1, y2, y3;
+  ld256g(x, x0, x1, x2, x3);
+  ld256g(y, y0, y1, y2, y3);
+  st256g(d, add_mod(x0, y0, p), add_mod(x1, y1, p), add_mod(x2, y2, p), add_mod(x3, y3, p));
 }
 
 __global__ void copy_kernel(View dst, u32 dst_lane0, View src, LaneMap sm, u32 nlanes, u32 comps,
@@ -478,7 +478,7 @@ cudaError_t launch_cmult(View out, u32 out_lane0, View a, LaneMap ma, View b, La
 
 cudaError_t launch_cadd(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, bool acc,
                         u32 nlanes, u32 comps, u32 limbs, u32 n, const PrimeConst* pc, cudaStream_t st) {
-  const u32 cpr = chunks_of(n);
+  const u32 cpr = (n + 1023) / 1024;
   const size_t g = (size_t)nlanes * comps * limbs * cpr;
   if (!g) return cudaSuccess;
   cadd_kernel<<<(unsigned)g, kThreads, 0, st>>>(out, out_lane0, a, ma, b, mb, acc ? 1 : 0, nlanes, comps,
