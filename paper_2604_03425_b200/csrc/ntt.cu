@@ -412,6 +412,10 @@ cudaError_t dispatch_pass(int logm, const NttLaunch& L, int kA, int kB, u32 rows
 namespace v2 {
 
 constexpr int kStride = 273;  // 256 + 16 + 1 padded words per sub-transform
+#ifndef AEGIS_CONV_TARGETS
+#define AEGIS_CONV_TARGETS 2
+#endif
+constexpr int kConvTargets = AEGIS_CONV_TARGETS;  // conversion targets per cfwd_a CTA
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 // Pass-B twiddle blob (built by ntt_build_blob, one contiguous block per tile
 // so a single TMA bulk copy stages it): per sub, round-2 twiddles stored
@@ -584,23 +588,46 @@ __device__ __forceinline__ void tile_fwd_a(const NttLaunch& L, RowRef rr, u32 ch
   for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
 }
 
-// fused exact conversion + forward pass A (target slot `slot` of lane `lane`):
-// the input of each element is computed from the k+1 prepared source tiles
-// (launch_conv_prep: xt_i and v in 24-bit split form) as
-// S = sum_i xt_i [B/b_i]_t + v (t - [B]_t), lazily reduced to [0, 3t).
-template <int K>
-__device__ __forceinline__ void tile_cfwd_a(const NttLaunch& L, const NttConvIn& C, u32 lane, u32 slot, u32 chunk,
-                                            double* sm) {
-  const RowRef rr = row_ref(L, lane, slot);
-  const NttScale* sc = L.scale + rr.prime;
-  const double p = sc->pd, pinv = sc->pinv;
+// forward pass A of one column chunk, input already in registers (lazy)
+__device__ __forceinline__ void pass_a_body(double (&x)[16], const double* tw, double p, double pinv, double* sm,
+                                            u64* col) {
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  double w[15];
+  load_w<0>(w, tw, 1, 0);
+  ct16(x, WArr{w}, p, pinv);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sm[lo * kStride + hi + 17 * v] = x[v];
+  load_w<4>(w, tw, 1, hi);
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + 17 * hi + v];
+  ct16(x, WArr{w}, p, pinv);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
+}
+
+// fused exact conversion + forward pass A for T target slots slot0 .. slot0+nt-1
+// of lane `lane`: every prepared source word (launch_conv_prep: x~_i and v in
+// 24-bit split form) is read once from L2 and feeds all T targets,
+//   S_t = sum_i x~_i [B/b_i]_t + v (t - [B]_t),
+// lazily reduced into [0, 3t).  Target 0 stays in registers; targets 1.. are
+// parked in this thread's private SMEM slots (`hand`) until their pass runs.
+template <int K, int T>
+__device__ __forceinline__ void tile_cfwd_a(const NttLaunch& L, const NttConvIn& C, u32 lane, u32 slot0, u32 nt,
+                                            u32 chunk, double* sm, u64* hand) {
   const ConvPlanDev* pl = C.plan;
   const u32 m = pl->m;
-  const u64 d = pl->dst_p[slot], mu = pl->dst_mu96[slot];
-  Split hs[K + 1];
+  Split hs[T][K + 1];
+  u64 dd[T], mu[T];
 #pragma unroll
-  for (int i = 0; i < K; ++i) hs[i] = split24(__ldg(C.hat_tab + (size_t)i * m + slot));
-  hs[K] = split24(d - pl->b_mod[slot]);
+  for (int t = 0; t < T; ++t) {
+    const u32 slot = slot0 + ((u32)t < nt ? t : 0);
+    dd[t] = pl->dst_p[slot];
+    mu[t] = pl->dst_mu96[slot];
+#pragma unroll
+    for (int i = 0; i < K; ++i) hs[t][i] = split24(__ldg(C.hat_tab + (size_t)i * m + slot));
+    hs[t][K] = split24(dd[t] - pl->b_mod[slot]);
+  }
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
   const size_t col0 = (size_t)chunk * 16 + lo + ((size_t)hi << 8);
   const uint2* ps[K + 1];
@@ -611,31 +638,34 @@ __device__ __forceinline__ void tile_cfwd_a(const NttLaunch& L, const NttConvIn&
   double x[16];
 #pragma unroll
   for (int v = 0; v < 16; ++v) {
-    Acc3 a;
+    uint2 w[K + 1];
 #pragma unroll
-    for (int i = 0; i <= K; ++i) {
-      const uint2 w = __ldg(ps[i] + (v << 12));
-      mac24(a, Split{w.x, w.y}, hs[i]);
+    for (int i = 0; i <= K; ++i) w[i] = __ldg(ps[i] + (v << 12));
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      Acc3 a;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) mac24(a, Split{w[i].x, w[i].y}, hs[t][i]);
+      // q = floor((S >> 32) floor(2^96/d) / 2^64) is within 3 below S/d: r = S - q d in [0, 3d)
+      const u64 top = (a.c2 << 16) + (a.c1 >> 8) + (a.c0 >> 32);
+      const u64 q = __umul64hi(top, mu[t]);
+      const u64 r = a.c0 + (a.c1 << 24) + (a.c2 << 48) - q * dd[t];
+      if (t == 0) x[v] = u2d(r);
+      else hand[(size_t)(t - 1) * 4096 + v * 256 + threadIdx.x] = r;
     }
-    // q = floor((S >> 32) floor(2^96/d) / 2^64) is within 3 below S/d: r = S - q d in [0, 3d)
-    const u64 top = (a.c2 << 16) + (a.c1 >> 8) + (a.c0 >> 32);
-    const u64 q = __umul64hi(top, mu);
-    const u64 s_lo = a.c0 + (a.c1 << 24) + (a.c2 << 48);
-    x[v] = u2d(s_lo - q * d);
   }
-  double w[15];
-  load_w<0>(w, L.tw[rr.prime].fw, 1, 0);
-  ct16(x, WArr{w}, p, pinv);
 #pragma unroll
-  for (int v = 0; v < 16; ++v) sm[lo * kStride + hi + 17 * v] = x[v];
-  load_w<4>(w, L.tw[rr.prime].fw, 1, hi);
-  __syncthreads();
+  for (int t = 0; t < T; ++t) {
+    if ((u32)t >= nt) break;
+    const RowRef rr = row_ref(L, lane, slot0 + t);
+    const NttScale* sc = L.scale + rr.prime;
+    if (t > 0) {
+      __syncthreads();  // sm (exchange rows) is reused by the next target
 #pragma unroll
-  for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + 17 * hi + v];
-  ct16(x, WArr{w}, p, pinv);
-  u64* col = rr.ptr + chunk * 16 + lo;
-#pragma unroll
-  for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
+      for (int v = 0; v < 16; ++v) x[v] = u2d(hand[(size_t)(t - 1) * 4096 + v * 256 + threadIdx.x]);
+    }
+    pass_a_body(x, L.tw[rr.prime].fw, sc->pd, sc->pinv, sm, rr.ptr + chunk * 16 + lo);
+  }
 }
 
 // forward pass B: block b = chunk*16 + hi (256 contiguous), tau = lo.  lazy in,
@@ -858,11 +888,13 @@ __global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
 
 // fused conversion + pass A, one launch per pass: tiles ordered (lane, chunk,
 // slot fastest) so the CTAs converting one lane's column chunk run together
-template <int K>
+template <int K, int T>
 __global__ void __launch_bounds__(256, 3) cfwd_a(const NttLaunch L, const NttConvIn C) {
-  __shared__ double sm[16 * kStride];
-  const u32 slot = blockIdx.x % L.nslots, rest = blockIdx.x / L.nslots;
-  tile_cfwd_a<K>(L, C, rest >> 4, slot, rest & 15, sm);
+  extern __shared__ double dyn[];  // exchange rows + (T-1) x 4096 parked targets
+  const u32 groups = (L.nslots + T - 1) / T;
+  const u32 grp = blockIdx.x % groups, rest = blockIdx.x / groups;
+  const u32 slot0 = grp * T, nt = L.nslots - slot0 < (u32)T ? L.nslots - slot0 : (u32)T;
+  tile_cfwd_a<K, T>(L, C, rest >> 4, slot0, nt, rest & 15, dyn, reinterpret_cast<u64*>(dyn + 16 * kStride));
 }
 
 void init_attrs() {
@@ -871,6 +903,11 @@ void init_attrs() {
     cudaFuncSetAttribute(fwd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     cudaFuncSetAttribute(inv_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     cudaFuncSetAttribute(fwd_b_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
+    const int cs = (int)((16 * kStride) * sizeof(double) + (kConvTargets - 1) * 4096 * sizeof(u64));
+    cudaFuncSetAttribute(cfwd_a<1, kConvTargets>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
+    cudaFuncSetAttribute(cfwd_a<2, kConvTargets>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
+    cudaFuncSetAttribute(cfwd_a<3, kConvTargets>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
+    cudaFuncSetAttribute(cfwd_a<4, kConvTargets>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
     init = true;
   }
 }
@@ -892,11 +929,14 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
 cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, cudaStream_t st) {
   init_attrs();
   const dim3 grid(L.nlanes * L.nslots * 16), block(256);
+  constexpr int T = kConvTargets;
+  const size_t smem = (size_t)(16 * kStride) * sizeof(double) + (size_t)(T - 1) * 4096 * sizeof(u64);
+  const dim3 cgrid(L.nlanes * 16 * ((L.nslots + T - 1) / T));
   switch (C.k) {
-    case 1: cfwd_a<1><<<grid, block, 0, st>>>(L, C); break;
-    case 2: cfwd_a<2><<<grid, block, 0, st>>>(L, C); break;
-    case 3: cfwd_a<3><<<grid, block, 0, st>>>(L, C); break;
-    case 4: cfwd_a<4><<<grid, block, 0, st>>>(L, C); break;
+    case 1: cfwd_a<1, T><<<cgrid, block, smem, st>>>(L, C); break;
+    case 2: cfwd_a<2, T><<<cgrid, block, smem, st>>>(L, C); break;
+    case 3: cfwd_a<3, T><<<cgrid, block, smem, st>>>(L, C); break;
+    case 4: cfwd_a<4, T><<<cgrid, block, smem, st>>>(L, C); break;
     default: return cudaErrorInvalidValue;
   }
   if (fin) fwd_b_fin<<<grid, block, kSmemB, st>>>(L, *fin);
