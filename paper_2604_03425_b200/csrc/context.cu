@@ -462,10 +462,11 @@ void Context::basis_convert(const u64* src, size_t src_ls, const std::vector<u32
 // sources are clobbered either way (callers pass scratch limbs).
 bool Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
                        u64* dst, size_t dst_ls, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
-                       u32 lanes, u64* vbuf, const NttFin* fin) {
+                       u32 lanes, u64* vbuf, const NttFin* fin, bool lazy_out) {
   const bool fused = log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2 && g_conv_fused && src_off.size() <= 4 &&
                      dst_off.size() <= (size_t)kMaxSlots && vbuf != nullptr;
   if (!fused) {
+    if (lazy_out) throw Error(AEGIS_ELOGIC, "lazy NTT outputs need the fused conversion path");
     basis_convert(src, src_ls, src_off, src_ext, dst, dst_ls, dst_off, dst_ext, lanes);
     ntt(dst, dst_ls, lanes, dst_off, dst_ext, false);
     return false;
@@ -491,6 +492,7 @@ bool Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off,
   }
   L.tw = d_tw;
   L.scale = d_scale;
+  L.lazy_out = lazy_out ? 1u : 0u;
   NttConvIn c;
   std::memset(&c, 0, sizeof(c));
   c.plan = pl.dev;
@@ -552,7 +554,7 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
           t_ext.push_back(t < l ? t : kSpecialBase + (t - l));
         }
       u64* ej = ext + (size_t)l0 * ext_ls + (size_t)(j * S.ns - lo) * n;
-      conv_ntt(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb, vbuf);
+      conv_ntt(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb, vbuf, nullptr, modup_lazy());
     }
   }
   release(dc);
@@ -611,6 +613,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
     km.d_lane_stride = d_ls;
     km.acc = acc;
     km.acc_lane_stride = acc_ls;
+    km.ext_lazy = modup_lazy() ? 1u : 0u;
     AEGIS_CHECK_CUDA(launch_keymul(km, nb, n, d_pc, stream));
     count();
     // ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}

@@ -99,7 +99,12 @@ class Context {
   // (returns true); otherwise dst holds the NTT and the caller finishes.
   bool conv_ntt(u64* src, size_t src_lane_stride, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
                 u64* dst, size_t dst_lane_stride, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
-                u32 lanes, u64* vbuf, const NttFin* fin = nullptr);
+                u32 lanes, u64* vbuf, const NttFin* fin = nullptr, bool lazy_out = false);
+  // ModUp outputs are left lazy (FP64 bits) when the fused conversion and the
+  // FP64 key product are both active: the key product is their only reader
+  bool modup_lazy() const {
+    return log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2 && g_conv_fused && g_km_f64;
+  }
   // Hybrid key switch (poly_ir.hpp:219-298) of `lanes` polynomials d (level
   // limbs each, NTT domain, lane stride d_ls).  out_c = add_c + KS_c(d).
   struct KsOut {

@@ -316,10 +316,12 @@ __global__ void __launch_bounds__(256) keymul_dn_kernel(const KeyMulIO io, u32 l
   const u64* db = io.d + (size_t)lane * io.d_lane_stride + (size_t)slot * n + x;
   const bool main_slot = slot < io.level;
   u64 e[DN], k0[DN], k1[DN];
+  u32 own_mask = 0;
 #pragma unroll
   for (int j = 0; j < DN; ++j) {
     const u32 lo = j * kAlpha, hi = lo + kAlpha < io.level ? lo + kAlpha : io.level;
     const bool own = main_slot && slot >= lo && slot < hi;
+    own_mask |= own ? 1u << j : 0u;
     const u32 idx = j * io.nslots - lo + (slot < lo ? slot : slot - (hi - lo));
     e[j] = own ? db[0] : eb[(size_t)idx * n];
     k0[j] = __ldg(kb + (size_t)j * 2 * kslot_stride);
@@ -344,7 +346,10 @@ __global__ void __launch_bounds__(256) keymul_dn_kernel(const KeyMulIO io, u32 l
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int j = 0; j < DN; ++j) {
-    const double v = f64_of(e[j]), w0 = f64_of(k0[j]), w1 = f64_of(k1[j]);
+    // own-digit words are canonical u64 (d); ModUp words may be lazy FP64 bits
+    const bool lazy = io.ext_lazy && !(own_mask >> j & 1u);
+    const double v = lazy ? __longlong_as_double((long long)e[j]) : f64_of(e[j]);
+    const double w0 = f64_of(k0[j]), w1 = f64_of(k1[j]);
     s0 += f64_mulmod(v, w0, w0 * pinv, pd);
     s1 += f64_mulmod(v, w1, w1 * pinv, pd);
   }

@@ -105,6 +105,7 @@ struct KeyMulIO {
   const u64* key;        // [digit][comp][keyslot][n]
   u32 key_slots;         // chain + 4
   u32 level, dnum, nslots;   // nslots = level + 4
+  u32 ext_lazy;              // ext words are lazy FP64 bits (NttLaunch::lazy_out), F64 path only
   u32 slot_ext[kMaxConv + 8];  // ext prime of slot
   u32 slot_key[kMaxConv + 8];  // key slot of slot
 };

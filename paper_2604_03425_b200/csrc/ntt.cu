@@ -693,6 +693,12 @@ __device__ __forceinline__ void tile_fwd_b(const NttLaunch& L, RowRef rr, u32 ch
   for (int v = 0; v < 16; ++v) x[v] = sp[17 * lo + v];
   ct16(x, WArr{w}, p, pinv);
   u64* o = blk + 16 * lo;
+  if (L.lazy_out) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      st256(o + 4 * k, bitsd(x[4 * k]), bitsd(x[4 * k + 1]), bitsd(x[4 * k + 2]), bitsd(x[4 * k + 3]));
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     st256(o + 4 * k, canon(x[4 * k], p, pinv), canon(x[4 * k + 1], p, pinv), canon(x[4 * k + 2], p, pinv),

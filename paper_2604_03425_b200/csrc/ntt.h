@@ -46,6 +46,10 @@ struct NttLaunch {
   const u64* in_base;
   size_t in_lane_stride;
   u32 in_slot_off[kMaxSlots];
+  // forward (v2): leave the outputs lazy (raw FP64 bits, |x| < 2^51, congruent
+  // to the result) instead of canonical u64 -- for ModUp outputs that only the
+  // FP64 key product reads
+  u32 lazy_out;
 };
 
 // pass-B twiddle blob of one 16-sub tile at N = 2^16 (ntt.cu v2):
