@@ -153,6 +153,14 @@ __device__ __forceinline__ void st256g(u64* p, u64 a, u64 b, u64 c, u64 d) {
   asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
 
+// streaming (evict-first) variants for data touched once per kernel
+__device__ __forceinline__ void ld256cs(const u64* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+__device__ __forceinline__ void st256cs(u64* p, u64 a, u64 b, u64 c, u64 d) {
+  asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
 // ---- exact FP64 modular arithmetic (p < 2^46; see ntt.cu v2 for the bounds) ----
 constexpr double kF64Magic = 6755399441055744.0;  // 1.5 * 2^52: round on the DFMA pipe
 constexpr double kF64Two52 = 4503599627370496.0;

@@ -91,22 +91,32 @@ __global__ void cmult_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b
   }
 }
 
-// 4 contiguous coefficients per thread with 256-bit accesses (HBM-bound)
+// 8 contiguous coefficients per thread with 256-bit accesses (HBM-bound).
+// The accumulator / first operand streams (evict-first) so a wrapped second
+// operand (e.g. the 48 product lanes added into 1,536 score lanes) stays in L2.
 __global__ void __launch_bounds__(256) cadd_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb,
                                                    int acc, u32 nlanes, u32 comps, u32 limbs, u32 n,
                                                    const PrimeConst* __restrict__ pc, u32 cpr) {
   const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
   const u32 lb = row % limbs, rest = row / limbs, comp = rest % comps, l = rest / comps;
   const u64 p = pc[lb].p;
-  const u32 t = (chunk * 256 + threadIdx.x) * 4;
-  if (t >= n) return;
-  const u64* x = a.limb(ma.at(l, nlanes), comp, lb, n) + t;
-  u64* d = out.limb(out_lane0 + l, comp, lb, n) + t;
-  const u64* y = acc ? d : b.limb(mb.at(l, nlanes), comp, lb, n) + t;
-  u64 x0, x1, x2, x3, y0, y1, y2, y3;
-  ld256g(x, x0, x1, x2, x3);
-  ld256g(y, y0, y1, y2, y3);
-  st256g(d, add_mod(x0, y0, p), add_mod(x1, y1, p), add_mod(x2, y2, p), add_mod(x3, y3, p));
+  const u64* x = a.limb(ma.at(l, nlanes), comp, lb, n);
+  u64* d = out.limb(out_lane0 + l, comp, lb, n);
+  const u64* y = acc ? d : b.limb(mb.at(l, nlanes), comp, lb, n);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const u32 t = (chunk * 512 + k * 256 + threadIdx.x) * 4;
+    if (t >= n) return;
+    u64 x0, x1, x2, x3, y0, y1, y2, y3;
+    if (acc) {  // d += x: d streams, x (possibly wrapped) is kept in L2
+      ld256g(x + t, x0, x1, x2, x3);
+      ld256cs(y + t, y0, y1, y2, y3);
+    } else {
+      ld256cs(x + t, x0, x1, x2, x3);
+      ld256g(y + t, y0, y1, y2, y3);
+    }
+    st256cs(d + t, add_mod(x0, y0, p), add_mod(x1, y1, p), add_mod(x2, y2, p), add_mod(x3, y3, p));
+  }
 }
 
 __global__ void copy_kernel(View dst, u32 dst_lane0, View src, LaneMap sm, u32 nlanes, u32 comps,
@@ -483,7 +493,7 @@ cudaError_t launch_cmult(View out, u32 out_lane0, View a, LaneMap ma, View b, La
 
 cudaError_t launch_cadd(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, bool acc,
                         u32 nlanes, u32 comps, u32 limbs, u32 n, const PrimeConst* pc, cudaStream_t st) {
-  const u32 cpr = (n + 1023) / 1024;
+  const u32 cpr = (n + 2047) / 2048;
   const size_t g = (size_t)nlanes * comps * limbs * cpr;
   if (!g) return cudaSuccess;
   cadd_kernel<<<(unsigned)g, kThreads, 0, st>>>(out, out_lane0, a, ma, b, mb, acc ? 1 : 0, nlanes, comps,

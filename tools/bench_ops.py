@@ -42,6 +42,11 @@ def graph(which, lanes, rots):
         lvl = 25
         L += [f"B 0 {lanes} {lvl} 2 0 0 0 0 src", f"B 1 {lanes} {lvl} 2 1 0 0 0 sq"]
         L += [op(0, 4, 1, lanes, lvl, [0, 0]), op(1, 6, 1, lanes, lvl, [1])]
+    elif which == "caddw":  # score accumulation: 48 product lanes added (wrapped) into 1,536
+        lvl = 33
+        L[1] = "inputs 0 1"
+        L += [f"B 0 {lanes} {lvl} 2 0 0 0 0 acc", f"B 1 {max(1, lanes // 32)} {lvl} 2 0 0 0 0 prod"]
+        L.append(f"O 0 2 0 0 0 {lanes} 1 0 -1 0 {lvl} 0 0 1 1 0 {max(1, lanes // 32)}")
     elif which == "softrot":
         lvl = 30
         L += [f"B 0 {lanes} {lvl} 2 0 0 0 0 src", f"B 1 {lanes} {lvl} 2 2 0 0 0 rot"]
