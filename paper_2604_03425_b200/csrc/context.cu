@@ -102,6 +102,7 @@ Context::Context(const aegis_params& prm, int dev) {
   if (const char* v2 = std::getenv("AEGIS_NTT_V2")) g_ntt_v2 = std::string(v2) != "0";
   if (const char* cf = std::getenv("AEGIS_CONV_FUSED")) g_conv_fused = std::string(cf) != "0";
   if (const char* kf = std::getenv("AEGIS_KM_F64")) g_km_f64 = std::string(kf) != "0";
+  if (const char* ks = std::getenv("AEGIS_KM_SPLIT")) g_km_split = std::string(ks) != "0";
 
   for (u32 e = 0; e < kNumExt; ++e) {
     const u64 p = primes_[e];
@@ -462,11 +463,11 @@ void Context::basis_convert(const u64* src, size_t src_ls, const std::vector<u32
 // sources are clobbered either way (callers pass scratch limbs).
 bool Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
                        u64* dst, size_t dst_ls, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
-                       u32 lanes, u64* vbuf, const NttFin* fin, bool lazy_out) {
+                       u32 lanes, u64* vbuf, const NttFin* fin, bool lazy_out, bool pass_a_only) {
   const bool fused = log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2 && g_conv_fused && src_off.size() <= 4 &&
                      dst_off.size() <= (size_t)kMaxSlots && vbuf != nullptr;
   if (!fused) {
-    if (lazy_out) throw Error(AEGIS_ELOGIC, "lazy NTT outputs need the fused conversion path");
+    if (lazy_out || pass_a_only) throw Error(AEGIS_ELOGIC, "lazy / split NTT outputs need the fused conversion path");
     basis_convert(src, src_ls, src_off, src_ext, dst, dst_ls, dst_off, dst_ext, lanes);
     ntt(dst, dst_ls, lanes, dst_off, dst_ext, false);
     return false;
@@ -503,8 +504,8 @@ bool Context::conv_ntt(u64* src, size_t src_ls, const std::vector<u32>& src_off,
   c.k = pl.k;
   c.v = vbuf;
   c.v_ls = n;
-  AEGIS_CHECK_CUDA(ntt_conv_fwd(L, c, fin, stream));
-  count(2);
+  AEGIS_CHECK_CUDA(ntt_conv_fwd(L, c, fin, stream, pass_a_only));
+  count(pass_a_only ? 1 : 2);
   return fin != nullptr;
 }
 
@@ -524,7 +525,7 @@ Context::KsShape Context::ks_shape(u32 l) const {
   return s;
 }
 
-void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
+void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext, bool pass_a_only) {
   if (l == 0 || l > chain) throw Error(AEGIS_EINVAL, "key switch level out of range");
   const KsShape S = ks_shape(l);
   const size_t ext_ls = modup_words_per_lane(l);
@@ -554,14 +555,14 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext) {
           t_ext.push_back(t < l ? t : kSpecialBase + (t - l));
         }
       u64* ej = ext + (size_t)l0 * ext_ls + (size_t)(j * S.ns - lo) * n;
-      conv_ntt(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb, vbuf, nullptr, modup_lazy());
+      conv_ntt(dc, (size_t)l * n, s_off, s_ext, ej, ext_ls, t_off, t_ext, nb, vbuf, nullptr, modup_lazy(), pass_a_only);
     }
   }
   release(dc);
 }
 
 void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 l, const u64* kbase, u64 galois,
-                      const KsOut& o) {
+                      const KsOut& o, bool ext_pass_a) {
   const KsShape S = ks_shape(l);
   const u32 K = kAlpha, ns = S.ns;
   const size_t ext_ls = modup_words_per_lane(l), acc_ls = (size_t)2 * ns * n;
@@ -614,7 +615,29 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
     km.acc = acc;
     km.acc_lane_stride = acc_ls;
     km.ext_lazy = modup_lazy() ? 1u : 0u;
-    AEGIS_CHECK_CUDA(launch_keymul(km, nb, n, d_pc, stream));
+    if (ext_pass_a) {  // ModUp second pass fused with the key product (ntt.cu fwd_b_km)
+      KmB kb;
+      std::memset(&kb, 0, sizeof(kb));
+      kb.ext = km.ext;
+      kb.ext_ls = ext_ls;
+      kb.d = km.d;
+      kb.d_ls = d_ls;
+      kb.key = kbase;
+      kb.acc = acc;
+      kb.acc_ls = acc_ls;
+      kb.tw = d_tw;
+      kb.scale = d_scale;
+      kb.key_slots = key_slots();
+      kb.level = l;
+      kb.dnum = S.dn;
+      kb.nslots = ns;
+      kb.chain = chain;
+      kb.nlanes = nb;
+      kb.n = n;
+      AEGIS_CHECK_CUDA(ntt_fwd_b_keymul(kb, stream));
+    } else {
+      AEGIS_CHECK_CUDA(launch_keymul(km, nb, n, d_pc, stream));
+    }
     count();
     // ModDown: Intt the P limbs, exact lift P -> Q_l, Ntt, (acc - conv) * P^{-1}
     ntt(acc, acc_ls, nb, p_off, p_ext, true);
@@ -663,15 +686,18 @@ void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id,
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)2 << 30) / (ext_lane * 8)));
   u64* ext = alloc(ext_lane * B);
   const u64* kbase = key(key_id);
+  // not hoisted: ModUp's second NTT pass runs inside the key product (the
+  // ModUp limbs are never materialised)
+  const bool split = modup_lazy() && g_km_split;
   for (u32 l0 = 0; l0 < lanes; l0 += B) {
     const u32 nb = std::min(B, lanes - l0);
-    modup(d + (size_t)l0 * d_ls, d_ls, nb, l, ext);
+    modup(d + (size_t)l0 * d_ls, d_ls, nb, l, ext, split);
     KsOut ob = o;
     for (int c = 0; c < 2; ++c) {
       ob.out[c] = o.out[c] + (size_t)l0 * o.out_lane[c];
       if (o.add[c]) ob.add[c] = o.add[c] + (size_t)l0 * o.add_lane[c];
     }
-    ks_core(ext, d + (size_t)l0 * d_ls, d_ls, nb, l, kbase, galois, ob);
+    ks_core(ext, d + (size_t)l0 * d_ls, d_ls, nb, l, kbase, galois, ob, split);
   }
   release(ext);
 }

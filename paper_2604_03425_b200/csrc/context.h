@@ -99,7 +99,7 @@ class Context {
   // (returns true); otherwise dst holds the NTT and the caller finishes.
   bool conv_ntt(u64* src, size_t src_lane_stride, const std::vector<u32>& src_off, const std::vector<u32>& src_ext,
                 u64* dst, size_t dst_lane_stride, const std::vector<u32>& dst_off, const std::vector<u32>& dst_ext,
-                u32 lanes, u64* vbuf, const NttFin* fin = nullptr, bool lazy_out = false);
+                u32 lanes, u64* vbuf, const NttFin* fin = nullptr, bool lazy_out = false, bool pass_a_only = false);
   // ModUp outputs are left lazy (FP64 bits) when the fused conversion and the
   // FP64 key product are both active: the key product is their only reader
   bool modup_lazy() const {
@@ -124,9 +124,10 @@ class Context {
   // word offset (j * ns - first prime of D_j) * n  (own-digit slots are read from d)
   size_t modup_words_per_lane(u32 l) const { return ((size_t)ks_shape(l).dn * ks_shape(l).ns - l) * n; }
   // ext[lane][digit][compact slot][n] = Ntt(exact lift of Intt(d) digit j to slot t)
-  void modup(const u64* d, size_t d_ls, u32 lanes, u32 level, u64* ext);
+  // pass_a_only: leave each digit's first-pass intermediate in ext (for ks_core(ext_pass_a))
+  void modup(const u64* d, size_t d_ls, u32 lanes, u32 level, u64* ext, bool pass_a_only = false);
   void ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 level, const u64* key, u64 galois,
-               const KsOut& o);
+               const KsOut& o, bool ext_pass_a = false);
   u64 galois_of(int offset) const;
 
   // ---- HE operators --------------------------------------------------------

@@ -40,6 +40,7 @@ namespace aegis {
 int g_ntt_impl = kNttF64;
 int g_ntt_v2 = 1;
 int g_conv_fused = 1;
+int g_km_split = 1;
 
 namespace {
 
@@ -838,6 +839,107 @@ __device__ __forceinline__ void tile_inv_a(const NttLaunch& L, RowRef rr, u32 ch
   for (int v = 0; v < 16; ++v) col[(size_t)(hi + 16 * v) << 8] = canon(x[v], p, pinv);
 }
 
+// pass B of every ModUp digit of one (lane, slot, chunk) + key inner product (see KmB)
+__global__ void __launch_bounds__(256, 2) fwd_b_km(const KmB K) {
+  extern __shared__ double dyn[];
+  __shared__ u64 mbar;
+  double* sm = dyn;                          // exchange rows
+  double* stw = dyn + 16 * kStride;          // round-2 twiddle blob of (prime, chunk)
+  double* acc1 = stw + kNttBlobTile;         // comp-1 accumulators: 16 private words per thread
+  const u32 lane = blockIdx.x % K.nlanes, rest = blockIdx.x / K.nlanes;
+  const u32 chunk = rest & 15, t = rest >> 4;
+  const u32 e = t < K.level ? t : kSpecialBase + (t - K.level);
+  const NttScale* sc = K.scale + e;
+  const double p = sc->pd, pinv = sc->pinv;
+  blob_init(&mbar);
+  __syncthreads();
+  blob_issue(&mbar, stw, K.tw[e].fb + (size_t)chunk * kNttBlobTile);
+  bool blob_ready = false;
+  const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
+  const size_t s0 = (size_t)(chunk * 16 + hi) * 256 + 16 * lo;
+  const size_t kcomp = (size_t)K.key_slots * K.n;
+  const u32 ks = t < K.level ? t : K.chain + (t - K.level);
+  const u64* kb = K.key + (size_t)ks * K.n + s0;
+  double* sp = sm + hi * kStride;
+  double acc0[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    acc0[v] = 0.0;
+    acc1[v * 256 + threadIdx.x] = 0.0;
+  }
+  for (u32 j = 0; j < K.dnum; ++j) {
+    const u32 lo_j = j * kAlpha, hi_j = lo_j + kAlpha < K.level ? lo_j + kAlpha : K.level;
+    const bool own = t < K.level && t >= lo_j && t < hi_j;
+    double y[16];
+    if (own) {  // E_j(t) = d[t], already in the NTT domain
+      const u64* dr = K.d + (size_t)lane * K.d_ls + (size_t)t * K.n + s0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        u64 a, b, c, dd;
+        ld256(dr + 4 * k, a, b, c, dd);
+        y[4 * k] = u2d(a);
+        y[4 * k + 1] = u2d(b);
+        y[4 * k + 2] = u2d(c);
+        y[4 * k + 3] = u2d(dd);
+      }
+    } else {
+      const u32 idx = j * K.nslots - lo_j + (t < lo_j ? t : t - (hi_j - lo_j));
+      const u64* blk = K.ext + (size_t)lane * K.ext_ls + (size_t)idx * K.n + (size_t)(chunk * 16 + hi) * 256;
+#pragma unroll
+      for (int v = 0; v < 16; ++v) y[v] = dbits(blk[lo + 16 * v]);
+      double w[15];
+      load_w<0>(w, K.tw[e].fw, 256 + chunk * 16 + hi, 0);
+      ct16(y, WArr{w}, p, pinv);
+#pragma unroll
+      for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = y[v];
+      __syncwarp();
+      if (!blob_ready) {
+        blob_wait(&mbar, 0);
+        blob_ready = true;
+      }
+      load_w_blob(w, stw + hi * kNttBlobSub + lo);
+#pragma unroll
+      for (int v = 0; v < 16; ++v) y[v] = sp[17 * lo + v];
+      __syncwarp();  // the rows are rewritten by the next digit
+      ct16(y, WArr{w}, p, pinv);
+    }
+    const u64* k0 = kb + (size_t)j * 2 * kcomp;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u64 a, b, c, dd;
+      ld256(k0 + 4 * k, a, b, c, dd);
+      const double w0 = u2d(a), w1 = u2d(b), w2 = u2d(c), w3 = u2d(dd);
+      acc0[4 * k] += mm(y[4 * k], w0, w0 * pinv, p);
+      acc0[4 * k + 1] += mm(y[4 * k + 1], w1, w1 * pinv, p);
+      acc0[4 * k + 2] += mm(y[4 * k + 2], w2, w2 * pinv, p);
+      acc0[4 * k + 3] += mm(y[4 * k + 3], w3, w3 * pinv, p);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u64 a, b, c, dd;
+      ld256(k0 + kcomp + 4 * k, a, b, c, dd);
+      const u64 kk[4] = {a, b, c, dd};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double wk = u2d(kk[i]);
+        acc1[(4 * k + i) * 256 + threadIdx.x] += mm(y[4 * k + i], wk, wk * pinv, p);
+      }
+    }
+  }
+  if (!blob_ready) blob_wait(&mbar, 0);  // never leave the bulk copy in flight
+  u64* a0 = K.acc + (size_t)lane * K.acc_ls + (size_t)t * K.n + s0;
+  u64* a1 = a0 + (size_t)K.nslots * K.n;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    st256(a0 + 4 * k, canon(acc0[4 * k], p, pinv), canon(acc0[4 * k + 1], p, pinv), canon(acc0[4 * k + 2], p, pinv),
+          canon(acc0[4 * k + 3], p, pinv));
+    st256(a1 + 4 * k, canon(acc1[(4 * k) * 256 + threadIdx.x], p, pinv),
+          canon(acc1[(4 * k + 1) * 256 + threadIdx.x], p, pinv), canon(acc1[(4 * k + 2) * 256 + threadIdx.x], p, pinv),
+          canon(acc1[(4 * k + 3) * 256 + threadIdx.x], p, pinv));
+  }
+}
+constexpr size_t kSmemKm = (size_t)(16 * kStride + kNttBlobTile + 4096) * sizeof(double);
+
 constexpr size_t kSmemB = (size_t)(16 * kStride + kNttBlobTile) * sizeof(double);
 
 // ---- one-launch-per-pass kernels (slot-major rows) ---------------------------
@@ -909,6 +1011,7 @@ void init_attrs() {
     cudaFuncSetAttribute(fwd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     cudaFuncSetAttribute(inv_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
     cudaFuncSetAttribute(fwd_b_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemB);
+    cudaFuncSetAttribute(fwd_b_km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemKm);
     const int cs = (int)((16 * kStride) * sizeof(double) + (kConvTargets - 1) * 4096 * sizeof(u64));
     cudaFuncSetAttribute(cfwd_a<1, kConvTargets>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
     cudaFuncSetAttribute(cfwd_a<2, kConvTargets>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
@@ -932,7 +1035,13 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, cudaStream_t st) {
+cudaError_t run_km(const KmB& K, cudaStream_t st) {
+  init_attrs();
+  fwd_b_km<<<K.nlanes * 16 * K.nslots, 256, kSmemKm, st>>>(K);
+  return cudaGetLastError();
+}
+
+cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, cudaStream_t st, bool pass_a_only) {
   init_attrs();
   const dim3 grid(L.nlanes * L.nslots * 16), block(256);
   constexpr int T = kConvTargets;
@@ -945,6 +1054,7 @@ cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, 
     case 4: cfwd_a<4, T><<<cgrid, block, smem, st>>>(L, C); break;
     default: return cudaErrorInvalidValue;
   }
+  if (pass_a_only) return cudaGetLastError();
   if (fin) fwd_b_fin<<<grid, block, kSmemB, st>>>(L, *fin);
   else fwd_b<<<grid, block, kSmemB, st>>>(L);
   return cudaGetLastError();
@@ -991,9 +1101,14 @@ void ntt_build_blob(const double* tab, double* blob) {
     }
 }
 
-cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, const NttFin* fin, cudaStream_t st) {
+cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, const NttFin* fin, cudaStream_t st,
+                         bool pass_a_only) {
   if (L.nlanes * L.nslots == 0) return cudaSuccess;
-  return v2::run_conv(L, c, fin, st);
+  return v2::run_conv(L, c, fin, st, pass_a_only);
+}
+cudaError_t ntt_fwd_b_keymul(const KmB& k, cudaStream_t st) {
+  if (!k.nlanes || !k.nslots) return cudaSuccess;
+  return v2::run_km(k, st);
 }
 cudaError_t ntt_fwd_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) {
   if (L.nlanes * L.nslots == 0) return cudaSuccess;

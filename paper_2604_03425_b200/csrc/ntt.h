@@ -28,6 +28,7 @@ enum NttImpl : int { kNttInt = 0, kNttF64 = 1 };
 extern int g_ntt_impl;  // selected at context creation (AEGIS_NTT_IMPL=int|f64)
 extern int g_ntt_v2;      // N = 2^16 FP64 passes with direct global access (AEGIS_NTT_V2=0 disables)
 extern int g_conv_fused;  // fused conversion + NTT (AEGIS_CONV_FUSED=0 disables)
+extern int g_km_split;    // non-hoisted KS: ModUp pass B fused into the key product (AEGIS_KM_SPLIT=0 disables)
 
 constexpr int kMaxSlots = 96;
 
@@ -89,9 +90,26 @@ struct NttFin {
   u32 log_n;
   u64 f[kMaxSlots];
 };
-cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, const NttFin* fin, cudaStream_t st);
+cudaError_t ntt_conv_fwd(const NttLaunch& L, const NttConvIn& c, const NttFin* fin, cudaStream_t st,
+                         bool pass_a_only = false);
 // plain forward NTT with the finish epilogue (sources already converted)
 cudaError_t ntt_fwd_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st);
+
+// Second forward pass of the ModUp NTTs fused with the key inner product
+// (non-hoisted key switching): for slot t of `lane`, each digit's pass-A
+// intermediate (compact ModUp layout, written by ntt_conv_fwd with pass_a_only)
+// is finished in registers and multiplied into the two key components;
+// acc[lane][c][t] = sum_j E_j(t) * key[j][c][t] is the only output.
+struct KmB {
+  const u64* ext; size_t ext_ls;  // pass-A intermediates, lazy FP64 bits
+  const u64* d; size_t d_ls;      // own-digit limbs (NTT domain, canonical)
+  const u64* key;                 // [digit][comp][keyslot][n]
+  u64* acc; size_t acc_ls;        // [lane][comp][slot][n]
+  const PrimeTw* tw;
+  const NttScale* scale;
+  u32 key_slots, level, dnum, nslots, chain, nlanes, n;
+};
+cudaError_t ntt_fwd_b_keymul(const KmB& k, cudaStream_t st);
 
 // true when ntt_run uses the v2 passes (out-of-place inverse, fused epilogues available)
 bool ntt_v2_active(int log_n);
