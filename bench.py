@@ -91,7 +91,9 @@ def dist_init(n_gpus):
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl" if os.environ.get("AEGIS_BACKEND", "nccl") == "nccl" else "gloo")
-        return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        # AEGIS_FORCE_DEVICE: run every rank on one GPU (multi-process path check on a 1-GPU box, gloo)
+        return dist, dist.get_rank(), ws, int(os.environ.get("AEGIS_FORCE_DEVICE", local))
     return None, 0, 1, 0
 
 
