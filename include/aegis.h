@@ -157,6 +157,10 @@ int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* t
                            uint32_t* ranks_per_group, uint32_t* part);
 /* hoisted ModUp across the rotations of one source (bit-exact; default on) */
 int aegis_graph_set_hoisting(aegis_graph* g, int enable);
+/* dead-lane elimination (default off): output lanes no later op reads are not
+ * computed.  The graph's final bundle is bit-identical; hashes of bundles with
+ * dead lanes are not meaningful in this mode.  Reported as a separate variant. */
+int aegis_graph_set_dce(aegis_graph* g, int enable);
 /* per-op device times (CUDA events around every HeOp) of the next runs */
 int aegis_graph_set_profiling(aegis_graph* g, int enable);
 int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t* n);

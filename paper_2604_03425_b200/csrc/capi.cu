@@ -87,6 +87,7 @@ struct aegis_graph {
   aegis::ReduceFn reduce = nullptr;
   void* reduce_user = nullptr;
   int hoist = 1;
+  int dce = 0;
   uint64_t h2d = 0, d2h = 0;
   bool profile = false;
   std::vector<float> op_ms;
@@ -111,6 +112,7 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.reduce = g->reduce;
   opt.reduce_user = g->reduce_user;
   opt.hoist = g->hoist != 0;
+  opt.dce = g->dce != 0;
   if (g->profile) opt.op_ms = &g->op_ms;
   // no trim here: the arena keeps its mapping across runs (re-mapping ~130 GB
   // per layer run stalled the stream); key allocation trims on demand
@@ -559,6 +561,11 @@ int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t
   if (!g) return AEGIS_EINVAL;
   for (size_t i = 0; i < g->op_ms.size() && i < cap; ++i) ms[i] = g->op_ms[i];
   if (n) *n = g->op_ms.size();
+  return AEGIS_OK;
+}
+int aegis_graph_set_dce(aegis_graph* g, int enable) {
+  if (!g) return AEGIS_EINVAL;
+  g->dce = enable;
   return AEGIS_OK;
 }
 int aegis_graph_set_hoisting(aegis_graph* g, int enable) {

@@ -43,6 +43,47 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
   }
   if (o.shard && !o.shard->active()) o.shard = nullptr;
   find_hoist_groups();
+  if (o.dce) find_live_lanes();
+}
+
+// Backward pass: a lane is live if the final bundle contains it or a later op
+// reads it (emit_per_lane operand rule, he_ir.hpp:200-222; a PMult reads every
+// input lane of its token groups, taken conservatively as all input lanes).
+// Overwrites are not tracked, so the set is a superset of the truly needed lanes.
+void Executor::find_live_lanes() {
+  using K = hp::HeOpKind;
+  live.assign(g.bundles.size(), {});
+  for (size_t b = 0; b < g.bundles.size(); ++b) live[b].assign(g.bundles[b].lanes, 0);
+  if (g.ops.empty()) return;
+  std::fill(live[g.ops.back().out.bundle].begin(), live[g.ops.back().out.bundle].end(), 1);
+  for (int64_t i = (int64_t)g.ops.size() - 1; i >= 0; --i) {
+    const hp::HeOp& op = g.ops[i];
+    if (op.kind == K::kEncode) continue;
+    const u32 n = op.out.lane_count;
+    const std::vector<char>& lo = live[op.out.bundle];
+    bool any = false;
+    for (u32 l = 0; l < n; ++l) any = any || lo[op.out.lane + l];
+    if (!any) continue;
+    for (const hp::LaneSlice& s : op.ins) {
+      if (g.bundles[s.bundle].components == 1 && op.kind == K::kPMult) continue;  // kGenerate weights
+      std::vector<char>& li = live[s.bundle];
+      if (op.kind == K::kPMult) {
+        for (u32 k = 0; k < s.lane_count; ++k) li[s.lane + k] = 1;
+        continue;
+      }
+      for (u32 l = 0; l < n; ++l)
+        if (lo[op.out.lane + l]) li[s.lane + (s.lane_count == n ? l : l % s.lane_count)] = 1;
+    }
+  }
+  // hoist groups: the source lanes any rotation of the group needs
+  for (size_t i = 0; i < g.ops.size(); ++i) {
+    if (group_of[i] < 0) continue;
+    const hp::HeOp& op = g.ops[i];
+    Group& gr = groups[group_of[i]];
+    if (gr.src_live.empty()) gr.src_live.assign(gr.count, 0);
+    for (u32 l = 0; l < op.out.lane_count && l < gr.count; ++l)
+      if (live[op.out.bundle][op.out.lane + l]) gr.src_live[l] = 1;
+  }
 }
 
 Executor::~Executor() {
@@ -161,6 +202,18 @@ void Executor::rot_run(const hp::HeOp& op, int64_t i, u32 pos, u32 len) {
     gr.prepared = true;
     gr.runs = o.shard ? o.shard->runs(gr.src, gr.lane0, gr.count)
                       : std::vector<std::pair<u32, u32>>{{gr.lane0, gr.lane0 + gr.count}};
+    if (o.dce && !gr.src_live.empty()) {  // only the source lanes some live rotation output needs
+      std::vector<std::pair<u32, u32>> lr;
+      for (auto [a, e] : gr.runs)
+        for (u32 x = a; x < e;) {
+          while (x < e && !gr.src_live[x - gr.lane0]) ++x;
+          u32 y = x;
+          while (y < e && gr.src_live[y - gr.lane0]) ++y;
+          if (x < y) lr.emplace_back(x, y);
+          x = y;
+        }
+      gr.runs = lr;
+    }
     u32 total = 0;
     for (auto [s, e] : gr.runs) {
       gr.run_off.push_back(total);
@@ -207,10 +260,21 @@ std::vector<std::pair<u32, u32>> Executor::out_runs(const hp::HeOp& op) const {
   std::vector<std::pair<u32, u32>> r;
   if (!o.shard) {
     r.emplace_back(0, n);
-    return r;
+  } else {
+    for (auto [s, e] : o.shard->runs(op.out.bundle, op.out.lane, n)) r.emplace_back(s - op.out.lane, e - op.out.lane);
   }
-  for (auto [s, e] : o.shard->runs(op.out.bundle, op.out.lane, n)) r.emplace_back(s - op.out.lane, e - op.out.lane);
-  return r;
+  if (!o.dce) return r;
+  std::vector<std::pair<u32, u32>> lr;  // dead-lane elimination: live output positions only
+  const std::vector<char>& lv = live[op.out.bundle];
+  for (auto [a, e] : r)
+    for (u32 x = a; x < e;) {
+      while (x < e && !lv[op.out.lane + x]) ++x;
+      u32 y = x;
+      while (y < e && lv[op.out.lane + y]) ++y;
+      if (x < y) lr.emplace_back(x, y);
+      x = y;
+    }
+  return lr;
 }
 
 // first position >= pos where a wrapped operand (count != n) wraps around

@@ -26,6 +26,7 @@ struct RunOptions {
   ReduceFn reduce = nullptr;
   void* reduce_user = nullptr;
   bool hoist = true;
+  bool dce = false;  // skip output lanes no later op reads (final bundle unchanged)
   std::vector<float>* op_ms = nullptr;  // if set: per-op device time (CUDA events)
 };
 
@@ -46,12 +47,15 @@ class Executor {
     std::vector<std::pair<u32, u32>> runs;  // owned source runs (absolute lanes)
     std::vector<u32> run_off;               // compact ext offset (lanes) of each run
     u32 hoisted = 0;                        // lanes (in run order) whose ModUp is cached
+    std::vector<char> src_live;             // dce: source lanes some rotation of the group needs
   };
 
   Bundle& get(u32 id);
   Bundle& input(const heplan::LaneSlice& s);
   void retire(u32 id);
   void find_hoist_groups();
+  void find_live_lanes();
+  bool live_lane(u32 b, u32 lane) const { return !o.dce || live[b][lane]; }
   size_t hoist_budget(size_t out_bytes);
   void step(const heplan::HeOp& op, int64_t i);
   void pmult(const heplan::HeOp& op);
@@ -71,6 +75,7 @@ class Executor {
   std::vector<int64_t> last_use;
   std::vector<Group> groups;
   std::vector<int> group_of;
+  std::vector<std::vector<char>> live;  // dce: [bundle][lane] read by a later op (or final)
   u32 final_bundle = 0xffffffffu;
 };
 

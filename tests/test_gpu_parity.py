@@ -416,3 +416,25 @@ def test_graph_parity_config1_production(golden_dir):
     h_gpu = g.run(max_ops=ops, hashes=True)
     h_cpu = orc(16).run_graph(path, max_ops=ops)
     assert (h_gpu[: len(h_cpu)] == h_cpu).all()
+
+
+@pytest.mark.parametrize("logn,tokens", [(11, 64), (11, 32)])
+def test_dead_lane_elimination_keeps_final_bundle(logn, tokens, tmp_path):
+    """The separately reported DCE variant skips rotated lanes no later op reads
+    (A.V consumes only the first out_lanes of each rotated
+    score bundle); the layer's output bundle must stay bit-identical."""
+    c = ctx(logn)
+    g = c.graph(kind=0, tokens=tokens)
+    path = str(tmp_path / "g.heops")
+    g.dump(path)
+    final = [int(ln.split()[4]) for ln in open(path) if ln.startswith("O ")][-1]
+    n0 = c.launch_count()
+    h = g.run(hashes=True)
+    n1 = c.launch_count()
+    g2 = c.graph(kind=0, tokens=tokens)
+    g2.set_dce(True)
+    h2 = g2.run(hashes=True)
+    n2 = c.launch_count()
+    assert h2[final] == h[final]
+    if tokens == 64:  # score lanes > A.V output lanes here: dead rotated lanes exist
+        assert n2 - n1 < n1 - n0  # ... and were skipped
