@@ -505,6 +505,14 @@ __device__ __forceinline__ void load_w_blob(double (&w)[15], const double* sp) {
 #pragma unroll
     for (int q = 0; q < (1 << sg); ++q) w[(1 << sg) - 1 + q] = sp[((1 << sg) - 1 + q) * 17];
 }
+// pass-B round-1 twiddles of one sub from the blob (half-warp broadcast)
+__device__ __forceinline__ void load_w_blob1(double (&w)[15], const double* sb) {
+#pragma unroll
+  for (int i = 0; i < 15; ++i) w[i] = sb[kTw1 + i];
+}
+#ifndef AEGIS_BLOB_R1
+#define AEGIS_BLOB_R1 1
+#endif
 struct WArr {
   const double* w;
   __device__ __forceinline__ double2 operator()(int sg, int q, double pinv) const {
@@ -681,14 +689,21 @@ __device__ __forceinline__ void tile_fwd_b(const NttLaunch& L, RowRef rr, u32 ch
   double x[16], w[15];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = dbits(blk[lo + 16 * v]);
+  const double* sb = stw + hi * kNttBlobSub;
+#if AEGIS_BLOB_R1
+  blob_wait(mbar, parity);
+  load_w_blob1(w, sb);
+#else
   load_w<0>(w, L.tw[rr.prime].fw, 256 + chunk * 16 + hi, 0);
+#endif
   ct16(x, WArr{w}, p, pinv);
   double* sp = sm + hi * kStride;
 #pragma unroll
   for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = x[v];
   __syncwarp();
+#if !AEGIS_BLOB_R1
   blob_wait(mbar, parity);
-  const double* sb = stw + hi * kNttBlobSub;
+#endif
   load_w_blob(w, sb + lo);
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sp[17 * lo + v];
@@ -717,13 +732,20 @@ __device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin&
   double x[16], w[15];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = dbits(blk[lo + 16 * v]);
+#if AEGIS_BLOB_R1
+  blob_wait(mbar, parity);
+  load_w_blob1(w, stw + hi * kNttBlobSub);
+#else
   load_w<0>(w, L.tw[rr.prime].fw, 256 + chunk * 16 + hi, 0);
+#endif
   ct16(x, WArr{w}, p, pinv);
   double* sp = sm + hi * kStride;
 #pragma unroll
   for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = x[v];
   __syncwarp();
+#if !AEGIS_BLOB_R1
   blob_wait(mbar, parity);
+#endif
   load_w_blob(w, stw + hi * kNttBlobSub + lo);
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sp[17 * lo + v];
@@ -808,7 +830,11 @@ __device__ __forceinline__ void tile_inv_b(const NttLaunch& L, RowRef rr, const 
   double* sp = sm + hi * kStride;
 #pragma unroll
   for (int v = 0; v < 16; ++v) sp[17 * lo + v] = red(x[v], p, pinv);
+#if AEGIS_BLOB_R1
+  load_w_blob1(w, sb);
+#else
   load_w<0>(w, L.tw[rr.prime].iw, 256 + chunk * 16 + hi, 0);
+#endif
   __syncwarp();
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = sp[lo + 17 * v];
@@ -888,7 +914,15 @@ __global__ void __launch_bounds__(256, 2) fwd_b_km(const KmB K) {
 #pragma unroll
       for (int v = 0; v < 16; ++v) y[v] = dbits(blk[lo + 16 * v]);
       double w[15];
+#if AEGIS_BLOB_R1
+      if (!blob_ready) {
+        blob_wait(&mbar, 0);
+        blob_ready = true;
+      }
+      load_w_blob1(w, stw + hi * kNttBlobSub);
+#else
       load_w<0>(w, K.tw[e].fw, 256 + chunk * 16 + hi, 0);
+#endif
       ct16(y, WArr{w}, p, pinv);
 #pragma unroll
       for (int v = 0; v < 16; ++v) sp[lo + 17 * v] = y[v];
