@@ -359,7 +359,12 @@ def ntt_roofline(c, st):
             "frac": achieved / pk.get("hbm_gbs"), "traffic": traffic,
             "peak_source": "measured" if not pk.get("_fallback") else "fallback",
             "ns_per_limb": t / limbs * 1e9,
-            "int_roofline_ns_per_limb": 524288 / 1.13e12 * 1e9}
+            # the binding resource of the 64-bit NTT on B200 is the FP64 pipe:
+            # 8 DFMA-pipe instructions per butterfly, 16 x 32768 butterflies per limb, plus the
+            # u64<->f64 conversions (~7 per coefficient); peak = 148 SMs x 64 lanes x max SM clock
+            "fp64_pipe": {"achieved_tops": limbs * (16 * 32768 * 8 + 7 * 65536) / t / 1e12,
+                          "peak_tops": 148 * 64 * 1.965e9 / 1e12,
+                          "frac": limbs * (16 * 32768 * 8 + 7 * 65536) / t / (148 * 64 * 1.965e9)}}
 
 
 def main():
