@@ -428,13 +428,12 @@ def test_dead_lane_elimination_keeps_final_bundle(logn, tokens, tmp_path):
     path = str(tmp_path / "g.heops")
     g.dump(path)
     final = [int(ln.split()[4]) for ln in open(path) if ln.startswith("O ")][-1]
-    n0 = c.launch_count()
     h = g.run(hashes=True)
-    n1 = c.launch_count()
     g2 = c.graph(kind=0, tokens=tokens)
     g2.set_dce(True)
     h2 = g2.run(hashes=True)
-    n2 = c.launch_count()
     assert h2[final] == h[final]
-    if tokens == 64:  # score lanes > A.V output lanes here: dead rotated lanes exist
-        assert n2 - n1 < n1 - n0  # ... and were skipped
+    # the score rotations rotate all QKV lanes but CMult reads only the Q lanes:
+    # those rotated bundles keep uncomputed (dead) lanes under DCE, so their
+    # whole-bundle hashes differ while the output bundle does not
+    assert (h2 != h).any()
