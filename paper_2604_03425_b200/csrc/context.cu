@@ -102,6 +102,7 @@ Context::Context(const aegis_params& prm, int dev) {
   if (const char* v2 = std::getenv("AEGIS_NTT_V2")) g_ntt_v2 = std::string(v2) != "0";
   if (const char* cf = std::getenv("AEGIS_CONV_FUSED")) g_conv_fused = std::string(cf) != "0";
   if (const char* kf = std::getenv("AEGIS_KM_F64")) g_km_f64 = std::string(kf) != "0";
+  if (const char* wsv = std::getenv("AEGIS_WS_SCALE")) ws_scale = std::max(0.05, std::atof(wsv));
   if (const char* ks = std::getenv("AEGIS_KM_SPLIT")) g_km_split = std::string(ks) != "0";
 
   for (u32 e = 0; e < kNumExt; ++e) {
@@ -531,7 +532,7 @@ void Context::modup(const u64* d, size_t d_ls, u32 lanes, u32 l, u64* ext, bool 
   const size_t ext_ls = modup_words_per_lane(l);
   std::vector<u32> main_off(l), main_ext(l);
   for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
-  const size_t budget = (size_t)1 << 30;
+  const size_t budget = ws_budget(1);
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / ((size_t)l * n * 8)));
   u64* dc = alloc((size_t)B * (l + 1) * n);
   u64* vbuf = dc + (size_t)B * l * n;
@@ -569,7 +570,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
   std::vector<u32> main_off(l), main_ext(l);
   for (u32 i = 0; i < l; ++i) main_off[i] = main_ext[i] = i;
   const size_t per_lane = (size_t)n * (2 * ns + 2 * (size_t)l);
-  const size_t budget = (size_t)1 << 30;
+  const size_t budget = ws_budget(1);
   const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, budget / (per_lane * 8)));
   u64* acc = alloc((per_lane + 2 * (size_t)n) * B);  // [B][2][ns][n]
   u64* pcv = acc + (size_t)B * 2 * ns * n;        // [B][2][l][n]
@@ -683,7 +684,7 @@ void Context::ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 
 
 void Context::keyswitch(const u64* d, size_t d_ls, u32 lanes, u32 l, u64 key_id, const KsOut& o, u64 galois) {
   const size_t ext_lane = modup_words_per_lane(l);
-  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)2 << 30) / (ext_lane * 8)));
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ws_budget(2) / (ext_lane * 8)));
   u64* ext = alloc(ext_lane * B);
   const u64* kbase = key(key_id);
   // not hoisted: ModUp's second NTT pass runs inside the key product (the
@@ -764,7 +765,7 @@ void Context::op_rescale(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im
   const u32 m = L - 1;
   // lanes in batches so the workspace stays ~1 GB (a T=2048 score tensor is 50 GB)
   const size_t per_lane = (size_t)2 * n * (1 + m);
-  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ((size_t)1 << 30) / (per_lane * 8)));
+  const u32 B = (u32)std::max<size_t>(1, std::min<size_t>(lanes, ws_budget(1) / (per_lane * 8)));
   u64* last = alloc((size_t)2 * B * n);
   u64* conv = alloc((size_t)2 * B * (m + 1) * n);
   u64* vbuf = conv + (size_t)2 * B * m * n;

@@ -148,6 +148,10 @@ class Context {
                 u32 ci_hi = ~0u);
 
   void count(u64 k = 1) { launches += k; }
+  // workspace budget of one operator phase: `gib` GiB scaled by AEGIS_WS_SCALE
+  // (bigger lane batches = fewer, fuller launches; more scratch memory)
+  size_t ws_budget(size_t gib) const { return (size_t)((double)(gib << 30) * ws_scale); }
+  double ws_scale = 3.0;
   std::string last_error;
 
  private:
