@@ -279,6 +279,22 @@ def run_aegis(args):
                        "T=2048, SURVEY Appendix B.5) are not computed; the layer output bundle is bit-identical "
                        "(tests/test_gpu_parity.py::test_dead_lane_elimination_keeps_final_bundle)"}
 
+    # ---- the other single-GPU BASELINE configs (parity cases, reported for reference) ----
+    others = None
+    if ws == 1 and not args.no_configs:
+        others = {}
+        for name, kind, tokens in (("config1_ffn_T128", 1, 128), ("config2_layer_T512", 0, 512)):
+            go = c.graph(kind=kind, tokens=tokens, layers=1)
+            c.keys_generate(go.key_ids())
+            go.run()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            go.run()
+            e1.record(st)
+            e1.synchronize()
+            others[name] = {"value": e0.elapsed_time(e1) / 1e3, "unit": "s/layer", "steps": 1}
+            go.free()
+
     # ---- roofline of the dominant kernel (batched NTT), timed on the library stream ----
     roof = ntt_roofline(c, st)
     out = None
@@ -301,6 +317,7 @@ def run_aegis(args):
             "clocks": clk.summary(),
             "peak_device_bytes": peak_bytes,
             "dce_variant": dce,
+            "other_configs": others,
         }
         print(json.dumps(out), flush=True)
     if dist:
@@ -378,6 +395,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dce", action="store_true", help="skip the dead-lane-elimination variant")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-1/2 reference timings")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
