@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].fb + (size_t)chunk * kNttBlobTile);
   tile_fwd_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
-__global__ void __launch_bounds__(256, 3) fwd_b_fin(const NttLaunch L, const NttFin F) {
+__global__ void __launch_bounds__(256, 2) fwd_b_fin(const NttLaunch L, const NttFin F) {
   extern __shared__ double dyn[];
   __shared__ u64 mbar;
   const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
