@@ -312,6 +312,53 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
 // words and 2*DN key words per thread are in flight together (the looped
 // form exposes one memory latency per digit).  Lanes vary fastest across the
 // grid so CTAs in flight share the key tile of one (slot, chunk) in L2.
+// Two adjacent coefficients per thread (128-bit loads and stores) for the
+// FP64 key product at DN <= 5 (the hoisted rotations at level 17): half the
+// load instructions for the same bytes in flight.
+template <int DN>
+__global__ void __launch_bounds__(256) keymul_dn2_kernel(const KeyMulIO io, u32 lanes, u32 n,
+                                                         const PrimeConst* __restrict__ pc) {
+  const u32 chunks = n / 512;
+  const u32 lane = blockIdx.x % lanes, rest = blockIdx.x / lanes;
+  const u32 chunk = rest % chunks, slot = rest / chunks;
+  const u32 x = (chunk * 256 + threadIdx.x) * 2;
+  const PrimeConst P = pc[io.slot_ext[slot]];
+  const size_t kslot_stride = (size_t)io.key_slots * n;
+  const u64* kb = io.key + (size_t)io.slot_key[slot] * n + x;
+  const u64* eb = io.ext + (size_t)lane * io.ext_lane_stride + x;
+  const u64* db = io.d + (size_t)lane * io.d_lane_stride + (size_t)slot * n + x;
+  const bool main_slot = slot < io.level;
+  ulonglong2 e[DN], k0[DN], k1[DN];
+  u32 own_mask = 0;
+#pragma unroll
+  for (int j = 0; j < DN; ++j) {
+    const u32 lo = j * kAlpha, hi = lo + kAlpha < io.level ? lo + kAlpha : io.level;
+    const bool own = main_slot && slot >= lo && slot < hi;
+    own_mask |= own ? 1u << j : 0u;
+    const u32 idx = j * io.nslots - lo + (slot < lo ? slot : slot - (hi - lo));
+    e[j] = *reinterpret_cast<const ulonglong2*>(own ? db : eb + (size_t)idx * n);
+    k0[j] = __ldg(reinterpret_cast<const ulonglong2*>(kb + (size_t)j * 2 * kslot_stride));
+    k1[j] = __ldg(reinterpret_cast<const ulonglong2*>(kb + (size_t)j * 2 * kslot_stride + kslot_stride));
+  }
+  const double pd = f64_of(P.p), pinv = 1.0 / pd;
+  double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
+#pragma unroll
+  for (int j = 0; j < DN; ++j) {
+    const bool lazy = io.ext_lazy && !(own_mask >> j & 1u);
+    const double va = lazy ? __longlong_as_double((long long)e[j].x) : f64_of(e[j].x);
+    const double vb = lazy ? __longlong_as_double((long long)e[j].y) : f64_of(e[j].y);
+    const double w0a = f64_of(k0[j].x), w0b = f64_of(k0[j].y), w1a = f64_of(k1[j].x), w1b = f64_of(k1[j].y);
+    s0a += f64_mulmod(va, w0a, w0a * pinv, pd);
+    s0b += f64_mulmod(vb, w0b, w0b * pinv, pd);
+    s1a += f64_mulmod(va, w1a, w1a * pinv, pd);
+    s1b += f64_mulmod(vb, w1b, w1b * pinv, pd);
+  }
+  u64* a0 = io.acc + (size_t)lane * io.acc_lane_stride + (size_t)slot * n + x;
+  *reinterpret_cast<ulonglong2*>(a0) = make_ulonglong2(f64_canon(s0a, pd, pinv), f64_canon(s0b, pd, pinv));
+  *reinterpret_cast<ulonglong2*>(a0 + (size_t)io.nslots * n) =
+      make_ulonglong2(f64_canon(s1a, pd, pinv), f64_canon(s1b, pd, pinv));
+}
+
 template <int DN, bool F64>
 __global__ void __launch_bounds__(256) keymul_dn_kernel(const KeyMulIO io, u32 lanes, u32 n,
                                                         const PrimeConst* __restrict__ pc) {
@@ -571,6 +618,17 @@ cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, con
 }
 
 cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  if (g_km_f64 && n >= 512 && io.dnum >= 1 && io.dnum <= 5) {
+    const size_t g = (size_t)lanes * io.nslots * (n / 512);
+    switch (io.dnum) {
+      case 1: keymul_dn2_kernel<1><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 2: keymul_dn2_kernel<2><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 3: keymul_dn2_kernel<3><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 4: keymul_dn2_kernel<4><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      default: keymul_dn2_kernel<5><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+    }
+    return cudaGetLastError();
+  }
   if (n >= 256 && io.dnum >= 1 && io.dnum <= 9) {
     const size_t g = (size_t)lanes * io.nslots * (n / 256);
 #define AEGIS_KM(D) \
