@@ -618,14 +618,18 @@ cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, con
 }
 
 cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst* pc, cudaStream_t st) {
-  if (g_km_f64 && n >= 512 && io.dnum >= 1 && io.dnum <= 5) {
+  if (g_km_f64 && n >= 512 && io.dnum >= 1 && io.dnum <= 9) {
     const size_t g = (size_t)lanes * io.nslots * (n / 512);
     switch (io.dnum) {
       case 1: keymul_dn2_kernel<1><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
       case 2: keymul_dn2_kernel<2><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
       case 3: keymul_dn2_kernel<3><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
       case 4: keymul_dn2_kernel<4><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      default: keymul_dn2_kernel<5><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 5: keymul_dn2_kernel<5><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 6: keymul_dn2_kernel<6><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 7: keymul_dn2_kernel<7><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 8: keymul_dn2_kernel<8><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      default: keymul_dn2_kernel<9><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
     }
     return cudaGetLastError();
   }

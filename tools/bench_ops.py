@@ -31,8 +31,8 @@ def op(i, kind, out, lanes, level, ins, rot=0, acc=0):
 
 def graph(which, lanes, rots):
     L = ["# heops v1 bench", "inputs 0"]
-    if which == "rot":
-        lvl = 17
+    if which in ("rot", "rot34"):
+        lvl = 17 if which == "rot" else 34
         L.append(f"B 0 {lanes} {lvl} 2 0 0 0 0 src")
         for r in range(rots):
             L.append(f"B {r + 1} {lanes} {lvl} 2 2 0 0 0 rot{r}")
@@ -85,7 +85,7 @@ def main():
             if os.environ.get("AEGIS_DEBUG"):
                 print("  host ms per run (enqueue):", hs)
             ms = min(ts)
-            units = a.lanes * (a.rots if w == "rot" else 1)
+            units = a.lanes * (a.rots if w.startswith("rot") else 1)
             print(f"{w:8s} {a.lanes} lanes: {ms:9.3f} ms/run  {ms * 1e3 / units:8.1f} us per lane-op "
                   f"(min of {a.reps}; all {[round(t, 1) for t in ts]})", flush=True)
 
