@@ -144,14 +144,14 @@ def _mini_graph(path, kind, level, lanes, c_in=0, c_out=0):
     open(path, "w").write("\n".join(L) + "\n")
 
 
-def cpu_baseline(args, budget_s=20.0):
+def cpu_baseline(args, budget_s=20.0, kind=0):
     """The CPU arm: the oracle (scalar C++ port of the reference semantics, all
     host threads) timed on single bundled ops of the layer's dominant kinds, then
     extrapolated over the layer's op list by per-kind lane x level costs."""
     from oracle_py import Oracle
     from paper_2604_03425_b200 import plan_graph
     threads = os.cpu_count() or 1
-    g = plan_graph(log_n=N_LOG, tokens=args.tokens, layers=1, kind=0)
+    g = plan_graph(log_n=N_LOG, tokens=args.tokens, layers=1, kind=kind)
     o = Oracle(N_LOG, threads=threads)
     meas = {}
     with tempfile.TemporaryDirectory() as d:
