@@ -260,20 +260,25 @@ def run_aegis(args):
     # ---- separately reported variant: dead-lane elimination (final bundle bit-identical) ----
     dce = None
     if not args.no_dce:
-        g.set_dce(True)
-        g.run()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        g.run()
-        e1.record(st)
-        e1.synchronize()
+        try:
+            g.set_dce(True)
+            g.run()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            g.run()
+            e1.record(st)
+            e1.synchronize()
+            dms = e0.elapsed_time(e1)
+        except Exception as exc:  # the variant must never cost the headline line
+            dms = float("nan")
+            dce = {"error": str(exc)[:200]}
         g.set_dce(False)
-        dms = e0.elapsed_time(e1)
         if dist:
             t = torch.tensor([dms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dms = float(t.item())
+    if not args.no_dce and dce is None:
         dce = {"value": dms / 1e3, "unit": "s/layer", "steps": 1,
                "note": "variant, not the headline: output lanes no later op reads (72.9% of the rotated lanes at "
                        "T=2048, SURVEY Appendix B.5) are not computed; the layer output bundle is bit-identical "
@@ -282,18 +287,8 @@ def run_aegis(args):
     # ---- the other single-GPU BASELINE configs (parity cases, reported for reference) ----
     others = None
     if ws == 1 and not args.no_configs:
-        others = {}
-        for name, kind, tokens in (("config1_ffn_T128", 1, 128), ("config2_layer_T512", 0, 512)):
-            go = c.graph(kind=kind, tokens=tokens, layers=1)
-            c.keys_generate(go.key_ids())
-            go.run()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            go.run()
-            e1.record(st)
-            e1.synchronize()
-            others[name] = {"value": e0.elapsed_time(e1) / 1e3, "unit": "s/layer", "steps": 1}
-            go.free()
+        others = {name: time_config(c, st, kind, tokens)
+                  for name, kind, tokens in (("config1_ffn_T128", 1, 128), ("config2_layer_T512", 0, 512))}
 
     # ---- roofline of the dominant kernel (batched NTT), timed on the library stream ----
     roof = ntt_roofline(c, st)
@@ -323,6 +318,25 @@ def run_aegis(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def time_config(c, st, kind, tokens):
+    """One warm + one timed run of another BASELINE config on this context
+    (reported for reference; a failure here never costs the headline line)."""
+    import torch
+    try:
+        go = c.graph(kind=kind, tokens=tokens, layers=1)
+        c.keys_generate(go.key_ids())
+        go.run()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        go.run()
+        e1.record(st)
+        e1.synchronize()
+        go.free()
+        return {"value": e0.elapsed_time(e1) / 1e3, "unit": "s/layer", "steps": 1}
+    except Exception as exc:
+        return {"error": str(exc)[:200]}
 
 
 def end_to_end(c, g, args, st, barrier):
