@@ -572,6 +572,7 @@ __device__ __forceinline__ RowRef row_ref(const NttLaunch& L, u32 lane, u32 slot
 }
 
 // forward pass A: columns c = chunk*16 + lo, thread tau = hi.  canonical in, lazy out.
+template <int KB = 8>  // column stride 2^KB (N = 2^(8+KB))
 __device__ __forceinline__ void tile_fwd_a(const NttLaunch& L, RowRef rr, u32 chunk, double* sm) {
   const double* tw = L.tw[rr.prime].fw;
   const NttScale* sc = L.scale + rr.prime;
@@ -581,7 +582,7 @@ __device__ __forceinline__ void tile_fwd_a(const NttLaunch& L, RowRef rr, u32 ch
   double x[16], w[15];
   u64 raw[16];
 #pragma unroll
-  for (int v = 0; v < 16; ++v) raw[v] = col[(size_t)(hi + 16 * v) << 8];
+  for (int v = 0; v < 16; ++v) raw[v] = col[(size_t)(hi + 16 * v) << KB];
   load_w<0>(w, tw, 1, 0);
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
@@ -594,7 +595,7 @@ __device__ __forceinline__ void tile_fwd_a(const NttLaunch& L, RowRef rr, u32 ch
   for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + 17 * hi + v];
   ct16(x, WArr{w}, p, pinv);
 #pragma unroll
-  for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << 8] = bitsd(x[v]);
+  for (int v = 0; v < 16; ++v) col[(size_t)(16 * hi + v) << KB] = bitsd(x[v]);
 }
 
 // forward pass A of one column chunk, input already in registers (lazy)
@@ -844,6 +845,7 @@ __device__ __forceinline__ void tile_inv_b(const NttLaunch& L, RowRef rr, const 
 }
 
 // inverse pass A (second): columns c = chunk*16 + lo, tau = hi; lazy in, canonical out, N^{-1} folded.
+template <int KB = 8>
 __device__ __forceinline__ void tile_inv_a(const NttLaunch& L, RowRef rr, u32 chunk, double* sm) {
   const NttScale* sc = L.scale + rr.prime;
   const double p = sc->pd, pinv = sc->pinv;
@@ -851,7 +853,7 @@ __device__ __forceinline__ void tile_inv_a(const NttLaunch& L, RowRef rr, u32 ch
   u64* col = rr.ptr + chunk * 16 + lo;
   double x[16], w[15];
 #pragma unroll
-  for (int v = 0; v < 16; ++v) x[v] = dbits(col[(size_t)(16 * hi + v) << 8]);
+  for (int v = 0; v < 16; ++v) x[v] = dbits(col[(size_t)(16 * hi + v) << KB]);
   load_w<4>(w, L.tw[rr.prime].iw, 1, hi);
   gs16<false>(x, WArr{w}, p, pinv, sc);
 #pragma unroll
@@ -862,7 +864,7 @@ __device__ __forceinline__ void tile_inv_a(const NttLaunch& L, RowRef rr, u32 ch
   for (int v = 0; v < 16; ++v) x[v] = sm[lo * kStride + hi + 17 * v];
   gs16<true>(x, WArr{w}, p, pinv, sc);
 #pragma unroll
-  for (int v = 0; v < 16; ++v) col[(size_t)(hi + 16 * v) << 8] = canon(x[v], p, pinv);
+  for (int v = 0; v < 16; ++v) col[(size_t)(hi + 16 * v) << KB] = canon(x[v], p, pinv);
 }
 
 // pass B of every ModUp digit of one (lane, slot, chunk) + key inner product (see KmB)
@@ -981,10 +983,11 @@ __device__ __forceinline__ RowRef slot_major(const NttLaunch& L, u32 row, u32& s
   slot = row / L.nlanes;
   return row_ref(L, row - slot * L.nlanes, slot);
 }
+template <int KB = 8>
 __global__ void __launch_bounds__(256, 3) fwd_a(const NttLaunch L) {
   __shared__ double sm[16 * kStride];
   u32 slot;
-  tile_fwd_a(L, slot_major(L, blockIdx.x >> 4, slot), blockIdx.x & 15, sm);
+  tile_fwd_a<KB>(L, slot_major(L, blockIdx.x >> (KB - 4), slot), blockIdx.x & ((1u << (KB - 4)) - 1), sm);
 }
 __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
   extern __shared__ double dyn[];
@@ -1022,10 +1025,11 @@ __global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].ib + (size_t)chunk * kNttBlobTile);
   tile_inv_b(L, rr, src, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
+template <int KB = 8>
 __global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
   __shared__ double sm[16 * kStride];
   u32 slot;
-  tile_inv_a(L, slot_major(L, blockIdx.x >> 4, slot), blockIdx.x & 15, sm);
+  tile_inv_a<KB>(L, slot_major(L, blockIdx.x >> (KB - 4), slot), blockIdx.x & ((1u << (KB - 4)) - 1), sm);
 }
 
 // fused conversion + pass A, one launch per pass: tiles ordered (lane, chunk,
@@ -1060,12 +1064,31 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
   const u32 rows = L.nlanes * L.nslots;
   const dim3 grid(rows * 16), block(256);
   if (!inverse) {
-    fwd_a<<<grid, block, 0, st>>>(L);
+    fwd_a<8><<<grid, block, 0, st>>>(L);
     fwd_b<<<grid, block, kSmemB, st>>>(L);
   } else {
     inv_b<<<grid, block, kSmemB, st>>>(L);
-    inv_a<<<grid, block, 0, st>>>(L);
+    inv_a<8><<<grid, block, 0, st>>>(L);
   }
+  return cudaGetLastError();
+}
+
+// N = 2^17 = 256 x 512: v2 column pass (256-point sub-transforms on 512
+// columns) + the generic 512-point block pass; the lazy FP64 intermediate and
+// the twiddle tables are shared, so the two pass families compose.
+cudaError_t run17(const NttLaunch& L, bool inverse, cudaStream_t st) {
+  init_attrs();
+  const u32 rows = L.nlanes * L.nslots;
+  const dim3 grid(rows * 32), block(256);
+  if (!inverse) {
+    fwd_a<9><<<grid, block, 0, st>>>(L);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_pass<9, 1, false, kNttF64>(L, 8, 9, rows, 0, st);
+  }
+  cudaError_t e = launch_pass<9, 1, true, kNttF64>(L, 8, 9, rows, 0, st);
+  if (e != cudaSuccess) return e;
+  inv_a<9><<<grid, block, 0, st>>>(L);
   return cudaGetLastError();
 }
 
@@ -1097,7 +1120,7 @@ cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, 
 cudaError_t run_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) {
   init_attrs();
   const dim3 grid(L.nlanes * L.nslots * 16), block(256);
-  fwd_a<<<grid, block, 0, st>>>(L);
+  fwd_a<8><<<grid, block, 0, st>>>(L);
   fwd_b_fin<<<grid, block, kSmemB, st>>>(L, fin);
   return cudaGetLastError();
 }
@@ -1155,6 +1178,7 @@ cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st
   if (L.nlanes * L.nslots == 0) return cudaSuccess;
   if (L.in_base && !(inverse && ntt_v2_active(log_n))) return cudaErrorInvalidValue;
   if (log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2) return v2::run(L, inverse, st);
+  if (log_n == 17 && g_ntt_impl == kNttF64 && g_ntt_v2 && !L.in_base) return v2::run17(L, inverse, st);
   return g_ntt_impl == kNttF64 ? run_impl<kNttF64>(L, log_n, inverse, st) : run_impl<kNttInt>(L, log_n, inverse, st);
 }
 
