@@ -1073,22 +1073,131 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// N = 2^17 = 256 x 512: v2 column pass (256-point sub-transforms on 512
-// columns) + the generic 512-point block pass; the lazy FP64 intermediate and
-// the twiddle tables are shared, so the two pass families compose.
+// ---- N = 2^17 block pass: 512-point sub-transforms (global stages 8..16) ----
+// A CTA owns 8 subs; warp w = sub w, lane = tau.  Rounds of 4, 4 and 1 stages
+// (element patterns tau + 32v, (tau&1) + 2v + 32(tau>>1), 16 tau + v), two
+// padded SMEM exchanges inside the warp.  Twiddles come from the w-only table:
+// round 1 uniform per warp, round 2 per lane pair, round 3 eight contiguous
+// words per lane (two 256-bit loads).  Input/output patterns are coalesced:
+// loads `tau + 32v` (forward) / 256-bit rows (inverse), stores the reverse.
+constexpr int kStride512 = 512 + 32 + 1;
+__device__ __forceinline__ u32 pad16(u32 u) { return u + (u >> 4); }
+
+__device__ __forceinline__ void load_w8(double (&w)[8], const double* tw, u32 t0, u32 tau) {
+  const u64* q = reinterpret_cast<const u64*>(tw + ((size_t)t0 << 8) + 8 * tau);
+  u64 a[8];
+  ld256(q, a[0], a[1], a[2], a[3]);
+  ld256(q + 4, a[4], a[5], a[6], a[7]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = dbits(a[k]);
+}
+
+__global__ void __launch_bounds__(256, 3) fwd_b512(const NttLaunch L) {
+  __shared__ double sm[8 * kStride512];
+  u32 slot;
+  const RowRef rr = slot_major(L, blockIdx.x >> 5, slot);
+  const u32 chunk = blockIdx.x & 31;
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
+  const double* tw = L.tw[rr.prime].fw;
+  const u32 tau = threadIdx.x & 31, sub = threadIdx.x >> 5;
+  const u32 t0 = 256 + chunk * 8 + sub, tl = tau & 1, th = tau >> 1;
+  u64* blk = rr.ptr + (size_t)(chunk * 8 + sub) * 512;
+  double x[16], w[15];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = dbits(blk[tau + 32 * v]);
+  load_w<0>(w, tw, t0, 0);
+  ct16(x, WArr{w}, p, pinv);
+  double* sp = sm + sub * kStride512;
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[pad16(tau + 32 * v)] = x[v];
+  __syncwarp();
+  load_w<4>(w, tw, t0, th);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[pad16(tl + 2 * v + 32 * th)];
+  ct16(x, WArr{w}, p, pinv);
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[pad16(tl + 2 * v + 32 * th)] = x[v];
+  __syncwarp();
+  double w8[8];
+  load_w8(w8, tw, t0, tau);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[pad16(16 * tau + v)];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double t = mm(x[2 * k + 1], w8[k], w8[k] * pinv, p);
+    const double a = x[2 * k];
+    x[2 * k] = a + t;
+    x[2 * k + 1] = a - t;
+  }
+  u64* o = blk + 16 * tau;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    st256(o + 4 * k, canon(x[4 * k], p, pinv), canon(x[4 * k + 1], p, pinv), canon(x[4 * k + 2], p, pinv),
+          canon(x[4 * k + 3], p, pinv));
+}
+
+__global__ void __launch_bounds__(256, 3) inv_b512(const NttLaunch L) {
+  __shared__ double sm[8 * kStride512];
+  u32 slot;
+  const RowRef rr = slot_major(L, blockIdx.x >> 5, slot);
+  const u32 chunk = blockIdx.x & 31;
+  const NttScale* sc = L.scale + rr.prime;
+  const double p = sc->pd, pinv = sc->pinv;
+  const double* tw = L.tw[rr.prime].iw;
+  const u32 tau = threadIdx.x & 31, sub = threadIdx.x >> 5;
+  const u32 t0 = 256 + chunk * 8 + sub, tl = tau & 1, th = tau >> 1;
+  u64* blk = rr.ptr + (size_t)(chunk * 8 + sub) * 512;
+  double x[16], w[15];
+  {
+    u64 raw[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ld256(blk + 16 * tau + 4 * k, raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = u2d(raw[v]);
+  }
+  double w8[8];
+  load_w8(w8, tw, t0, tau);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // GS stage 8
+    const double a = x[2 * k], b = x[2 * k + 1];
+    x[2 * k] = a + b;
+    x[2 * k + 1] = mm(a - b, w8[k], w8[k] * pinv, p);
+  }
+  double* sp = sm + sub * kStride512;
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[pad16(16 * tau + v)] = red(x[v], p, pinv);
+  __syncwarp();
+  load_w<4>(w, tw, t0, th);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[pad16(tl + 2 * v + 32 * th)];
+  gs16<false>(x, WArr{w}, p, pinv, sc);
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) sp[pad16(tl + 2 * v + 32 * th)] = red(x[v], p, pinv);
+  __syncwarp();
+  load_w<0>(w, tw, t0, 0);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = sp[pad16(tau + 32 * v)];
+  gs16<false>(x, WArr{w}, p, pinv, sc);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) blk[tau + 32 * v] = bitsd(red(x[v], p, pinv));
+}
+
+// N = 2^17 = 256 x 512: column pass (256-point sub-transforms on 512 columns)
+// + the 512-point block pass above.
 cudaError_t run17(const NttLaunch& L, bool inverse, cudaStream_t st) {
   init_attrs();
   const u32 rows = L.nlanes * L.nslots;
   const dim3 grid(rows * 32), block(256);
   if (!inverse) {
     fwd_a<9><<<grid, block, 0, st>>>(L);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return launch_pass<9, 1, false, kNttF64>(L, 8, 9, rows, 0, st);
+    fwd_b512<<<grid, block, 0, st>>>(L);
+  } else {
+    inv_b512<<<grid, block, 0, st>>>(L);
+    inv_a<9><<<grid, block, 0, st>>>(L);
   }
-  cudaError_t e = launch_pass<9, 1, true, kNttF64>(L, 8, 9, rows, 0, st);
-  if (e != cudaSuccess) return e;
-  inv_a<9><<<grid, block, 0, st>>>(L);
   return cudaGetLastError();
 }
 
