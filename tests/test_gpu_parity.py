@@ -445,3 +445,61 @@ def test_dead_lane_elimination_keeps_final_bundle(logn, tokens, tmp_path):
     # those rotated bundles keep uncomputed (dead) lanes under DCE, so their
     # whole-bundle hashes differ while the output bundle does not
     assert (h2 != h).any()
+
+
+def _small_batch_ctx():
+    """A production-size context whose operator workspaces hold 1-2 lanes, so
+    every lane-batch loop (ModUp, key product / ModDown, rescale) iterates."""
+    import os
+    from paper_2604_03425_b200 import Context
+    old = os.environ.get("AEGIS_WS_SCALE")
+    os.environ["AEGIS_WS_SCALE"] = "0.01"
+    try:
+        return Context(log_n=16)
+    finally:
+        if old is None:
+            del os.environ["AEGIS_WS_SCALE"]
+        else:
+            os.environ["AEGIS_WS_SCALE"] = old
+
+
+def test_multibatch_keyswitch_rescale_production():
+    """Rot / Relin / Rescale over 6 lanes at N = 2^16, l = 17 with 1-2 lanes per
+    batch: first, middle and last lanes bit-exact vs the oracle."""
+    c, o = _small_batch_ctx(), orc(16)
+    n, L = 1 << 16, 17
+    rng = np.random.default_rng(77)
+    x = rand_bundle(rng, 6, 2, L, n)
+    bi = upload(c, x)
+    br = c.bundle(6, 2, L)
+    c.rot(br, bi, 5, L)
+    got_r = br.download()
+    p3 = c.bundle(6, 3, L)
+    c.cmult(p3, bi, bi, L)
+    t = p3.download()
+    c.relin(p3, L)
+    got_l = p3.download()
+    bs = c.bundle(6, 2, L - 1)
+    c.rescale(bs, bi, L)
+    got_s = bs.download()
+    for ln in (0, 3, 5):
+        assert (got_r[ln] == o.rotate(x[ln], L, 5)).all(), ("rot", ln)
+        assert (got_l[ln, :2] == o.relin(t[ln], L)).all(), ("relin", ln)
+        assert (got_s[ln] == o.rescale(x[ln], L)).all(), ("rescale", ln)
+
+
+def test_multibatch_hoisted_rotations_production(tmp_path):
+    """Three hoisted rotations of one 6-lane source at N = 2^16, l = 17 through
+    the graph executor with 1-2 lanes per batch: bundle hashes vs the oracle."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from bench_ops import graph
+    path = str(tmp_path / "rot.heops")
+    open(path, "w").write(graph("rot", 6, 3))
+    c = _small_batch_ctx()
+    g = c.load_graph(path)
+    c.keys_generate(g.key_ids())
+    h_gpu = g.run(hashes=True)
+    h_cpu = orc(16).run_graph(path)
+    assert (h_gpu[: len(h_cpu)] == h_cpu).all()
