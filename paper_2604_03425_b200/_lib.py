@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaegis.so")
+# AEGIS_LIB: an alternate build of the same library (dev A/B of kernel variants)
+LIB_PATH = os.environ.get("AEGIS_LIB") or os.path.join(_HERE, "libaegis.so")
 
 u32 = ctypes.c_uint32
 u64 = ctypes.c_uint64

@@ -440,49 +440,73 @@ __global__ void finish_kernel(const FinishIO io, u32 n, const PrimeConst* __rest
 // Bundled PCMM step with in-kernel weights (kGenerate, poly_ir.hpp:57, 310-321)
 // ---------------------------------------------------------------------------
 constexpr u32 kPmTx = 32;      // coefficients per CTA
-constexpr u32 kPmGroups = 8;   // o-groups per CTA (256 threads)
+constexpr u32 kPmGroups = 8;   // max o-groups per CTA (256 threads)
+
+// o-groups per CTA: the largest divisor of c_out <= kPmGroups, so every
+// thread runs the same number of outputs (c_out = 12 -> 6 groups x 2)
+inline u32 pmult_groups(u32 c_out) {
+  for (u32 g = kPmGroups; g > 1; --g)
+    if (c_out % g == 0) return g;
+  return c_out < kPmGroups ? c_out : kPmGroups;
+}
 
 // acc lane for (token group t, output o') is acc_lane0 + t*c_out + o'; the
 // weight lane is ci*w_cout + o_off + o' (o_off/w_cout select one sub-tensor
 // of a chunked accumulator, CtBundle::chunk_period, he_ir.hpp:338).
-template <int TG>
-__global__ void __launch_bounds__(256) pmult_kernel(const PmultArgs a, const PrimeConst* __restrict__ pc) {
-  extern __shared__ Split xs[];  // [TG * c_in][2][kPmTx], pre-split into 24-bit limbs
+// SMEM: x tile pre-split into 24-bit limbs [TG * c_in][2][kPmTx], then this
+// limb's weight row keys [c_in][c_out] (read once per (ci, o) by a warp, so
+// the per-iteration key fetch is an LDS broadcast, not a dependent LDG).
+// MINB: resident CTAs the register budget targets -- 3 when SMEM allows it
+// (TG = 4 then spills a few words, still the faster trade), else 2.
+template <int TG, int MINB>
+__global__ void __launch_bounds__(256, MINB) pmult_kernel(const PmultArgs a, const PrimeConst* __restrict__ pc) {
+  extern __shared__ Split xs[];
   const u32 n = a.n, c_in = a.c_in, c_out = a.c_out, limbs = a.limbs;
   const u32 tiles = n / kPmTx;
   const u32 lb = blockIdx.x / tiles;
   const u32 x0 = (blockIdx.x - lb * tiles) * kPmTx;
   const PrimeConst P = pc[lb];
   const u32 nx = TG * c_in;
+  u64* rks = reinterpret_cast<u64*>(xs + nx * 2 * kPmTx);
+  for (u32 e = threadIdx.x; e < c_in * c_out; e += blockDim.x) {
+    const u32 ci = e / c_out, o = e - ci * c_out;
+    rks[e] = a.rowkeys[(size_t)((a.ci_off + ci) * a.w_cout + a.o_off + o) * limbs + lb];
+  }
   for (u32 e = threadIdx.x; e < nx * 2 * kPmTx; e += blockDim.x) {
     const u32 xx = e % kPmTx, r = e / kPmTx, comp = r & 1, ln = r >> 1;
     const u32 t = ln / c_in, ci = ln - t * c_in;
     xs[e] = split24(a.x.limb(a.x_lane0 + t * a.x_tstride + ci, comp, lb, n)[x0 + xx]);
   }
   __syncthreads();
+  const u32 groups = blockDim.x / kPmTx;
   const u32 xx = threadIdx.x % kPmTx;
   const u32 og = threadIdx.x / kPmTx;
   const u64 xi = x0 + xx;
-  const u64* __restrict__ rowkeys = a.rowkeys;
-  for (u32 o = og; o < c_out; o += kPmGroups) {
+  for (u32 o = og; o < c_out; o += groups) {
+    // the accumulator words are fetched before the MAC loop so their latency
+    // hides under it (the loads cannot move across the stores otherwise)
+    u64 prev[TG][2];
+#pragma unroll
+    for (int t = 0; t < TG; ++t)
+#pragma unroll
+      for (int cp = 0; cp < 2; ++cp) prev[t][cp] = a.acc.limb(a.acc_lane0 + t * a.acc_tstride + o, cp, lb, n)[xi];
     Acc3 s[TG][2];
+#pragma unroll 1
     for (u32 ci = 0; ci < c_in; ++ci) {
-      const u64 rk = rowkeys[(size_t)((a.ci_off + ci) * a.w_cout + a.o_off + o) * limbs + lb];
-      const Split w = split24(uniform_at(rk, xi, P.p, P.shift));
+      const Split w = split24(uniform_at(rks[ci * c_out + o], xi, P.p, P.shift));
 #pragma unroll
       for (int t = 0; t < TG; ++t) {
         const u32 r = (t * c_in + ci) * 2;
-        mac24(s[t][0], xs[r * kPmTx + xx], w);
-        mac24(s[t][1], xs[(r + 1) * kPmTx + xx], w);
+        mac24_ptx(s[t][0], xs[r * kPmTx + xx], w);
+        mac24_ptx(s[t][1], xs[(r + 1) * kPmTx + xx], w);
       }
     }
 #pragma unroll
     for (int t = 0; t < TG; ++t)
 #pragma unroll
       for (int cp = 0; cp < 2; ++cp) {
-        u64* d = a.acc.limb(a.acc_lane0 + t * a.acc_tstride + o, cp, lb, n) + xi;
-        s[t][cp].c0 += *d;
-        *d = acc3_reduce(s[t][cp], P.p, P.mu104);
+        s[t][cp].c0 += prev[t][cp];
+        a.acc.limb(a.acc_lane0 + t * a.acc_tstride + o, cp, lb, n)[xi] = acc3_reduce(s[t][cp], P.p, P.mu104);
       }
   }
 }
@@ -670,14 +694,16 @@ cudaError_t launch_weight_rowkeys(u64* out, u32 wlanes, u32 limbs, u64 seed, u64
 
 cudaError_t launch_pmult_acc(const PmultArgs& a, const PrimeConst* pc, cudaStream_t st) {
   if (a.n < kPmTx) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)a.tg * a.c_in * 2 * kPmTx * sizeof(u64);
+  const u32 tg4 = a.tg < 4 ? a.tg : 4;
+  const size_t smem = ((size_t)tg4 * a.c_in * 2 * kPmTx + (size_t)a.c_in * a.c_out) * sizeof(u64);
   const unsigned grid = a.limbs * (a.n / kPmTx);
+  const unsigned block = kPmTx * pmult_groups(a.c_out);
   if (!grid || !a.c_in || !a.c_out) return cudaSuccess;
 #define AEGIS_PM(TGV)                                                                          \
   case TGV: {                                                                                  \
-    auto kern = pmult_kernel<TGV>;                                                             \
+    auto kern = smem * 3 <= 220 * 1024 ? pmult_kernel<TGV, 3> : pmult_kernel<TGV, 2>;           \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    kern<<<grid, kPmTx * kPmGroups, smem, st>>>(a, pc);                                        \
+    kern<<<grid, block, smem, st>>>(a, pc);                                        \
     break;                                                                                     \
   }
   switch (a.tg) {

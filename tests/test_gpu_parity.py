@@ -276,7 +276,7 @@ def test_cadd_forms():
         assert (got2[ln] == (got[ln] + b[ln % 2, :, :3]) % q).all()
 
 
-@pytest.mark.parametrize("tg,c_in,c_out,chunk", [(1, 3, 4, 0), (2, 2, 3, 0), (2, 3, 6, 6), (5, 2, 2, 0)])
+@pytest.mark.parametrize("tg,c_in,c_out,chunk", [(1, 3, 4, 0), (2, 2, 3, 0), (2, 3, 6, 6), (5, 2, 2, 0), (1, 2, 9, 0), (4, 5, 7, 0)])
 def test_pmult_acc(tg, c_in, c_out, chunk):
     """Bundled PCMM step with in-kernel kGenerate weights."""
     c, o = ctx(10), orc(10)
