@@ -21,12 +21,15 @@ def main():
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-hoist", action="store_true")
+    ap.add_argument("--dce", action="store_true", help="dead-lane elimination variant")
     a = ap.parse_args()
     c = Context(log_n=16)
     g = c.graph(kind=0, tokens=a.tokens)
     c.keys_generate(g.key_ids())
     if a.no_hoist:
         g.set_hoisting(False)
+    if a.dce:
+        g.set_dce(True)
     g.run()  # warm
     g.set_profiling(True)
     g.run()
