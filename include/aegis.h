@@ -161,6 +161,12 @@ int aegis_graph_set_hoisting(aegis_graph* g, int enable);
  * computed.  The graph's final bundle is bit-identical; hashes of bundles with
  * dead lanes are not meaningful in this mode.  Reported as a separate variant. */
 int aegis_graph_set_dce(aegis_graph* g, int enable);
+/* wrapped accumulation (default on): accumulating CAdds whose operand is
+ * narrower than the output (acc[j] += x[j mod m]) are summed at the operand's
+ * width and applied to the output once, before its next reader.  Modular
+ * addition is exact and associative, so every bundle any op reads -- and every
+ * bundle hash -- is bit-identical to op-by-op execution. */
+int aegis_graph_set_wrap_defer(aegis_graph* g, int enable);
 /* per-op device times (CUDA events around every HeOp) of the next runs */
 int aegis_graph_set_profiling(aegis_graph* g, int enable);
 int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t* n);

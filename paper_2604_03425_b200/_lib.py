@@ -75,6 +75,7 @@ SIGNATURES = [
     ("aegis_graph_shard_info", ctypes.c_int, [vp, u32p, u32p, u32p, u32p, u32p]),
     ("aegis_graph_set_hoisting", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_graph_set_dce", ctypes.c_int, [vp, ctypes.c_int]),
+    ("aegis_graph_set_wrap_defer", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_graph_set_profiling", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_graph_op_times", ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_float), u64, u64p]),
     ("aegis_graph_io_bytes", ctypes.c_int, [vp, u64p, u64p]),

@@ -288,6 +288,10 @@ class Graph:
     def set_hoisting(self, enable):
         self.lib.aegis_graph_set_hoisting(self.h, 1 if enable else 0)
 
+    def set_wrap_defer(self, enable):
+        """Wrapped accumulating CAdds summed at the operand width (bit-identical; default on)."""
+        self.lib.aegis_graph_set_wrap_defer(self.h, 1 if enable else 0)
+
     def set_dce(self, enable):
         """Dead-lane elimination (separately reported variant; final bundle bit-identical)."""
         self.lib.aegis_graph_set_dce(self.h, 1 if enable else 0)

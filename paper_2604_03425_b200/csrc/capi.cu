@@ -88,6 +88,7 @@ struct aegis_graph {
   void* reduce_user = nullptr;
   int hoist = 1;
   int dce = 0;
+  int wrap_defer = 1;
   uint64_t h2d = 0, d2h = 0;
   bool profile = false;
   std::vector<float> op_ms;
@@ -113,6 +114,7 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.reduce_user = g->reduce_user;
   opt.hoist = g->hoist != 0;
   opt.dce = g->dce != 0;
+  opt.wrap_defer = g->wrap_defer != 0;
   if (g->profile) opt.op_ms = &g->op_ms;
   // no trim here: the arena keeps its mapping across runs (re-mapping ~130 GB
   // per layer run stalled the stream); key allocation trims on demand
@@ -566,6 +568,11 @@ int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t
 int aegis_graph_set_dce(aegis_graph* g, int enable) {
   if (!g) return AEGIS_EINVAL;
   g->dce = enable;
+  return AEGIS_OK;
+}
+int aegis_graph_set_wrap_defer(aegis_graph* g, int enable) {
+  if (!g) return AEGIS_EINVAL;
+  g->wrap_defer = enable;
   return AEGIS_OK;
 }
 int aegis_graph_set_hoisting(aegis_graph* g, int enable) {

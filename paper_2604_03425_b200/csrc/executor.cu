@@ -28,6 +28,8 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
   zero_first.assign(nb, 0);
   partial.assign(nb, 0);
   donated.assign(nb, 0);
+  shadow.assign(nb, nullptr);
+  shadow_level.assign(nb, 0);
   last_use.assign(nb, -1);
   std::vector<char> seen(nb, 0);
   for (size_t i = 0; i < nb; ++i) alloc_comps[i] = g.bundles[i].components;
@@ -89,6 +91,7 @@ void Executor::find_live_lanes() {
 Executor::~Executor() {
   for (auto& gr : groups)
     if (gr.ext) c.release(gr.ext);
+  for (Bundle* S : shadow) c.free_bundle(S);
   for (size_t i = 0; i < buf.size(); ++i)
     if (buf[i] && !donated[i]) c.free_bundle(buf[i]);
 }
@@ -103,12 +106,14 @@ Bundle& Executor::get(u32 id) {
 }
 
 Bundle& Executor::input(const hp::LaneSlice& s) {
+  if (shadow[s.bundle]) materialize(s.bundle);
   if (!buf[s.bundle]) throw Error(AEGIS_ELOGIC, "op reads bundle " + g.bundles[s.bundle].tag + " before it is written");
   if (partial[s.bundle]) reduce_partial(s.bundle);
   return *buf[s.bundle];
 }
 
 void Executor::retire(u32 id) {
+  if (shadow[id]) materialize(id);
   if (!buf[id]) return;
   if (donated[id]) {  // storage now belongs to the op's output bundle
     buf[id] = nullptr;
@@ -385,10 +390,53 @@ void Executor::donate(const hp::HeOp& op, int64_t i) {
   cur_comps[op.out.bundle] = 2;
 }
 
+// Wrapped accumulation (score.acc at T = 2048: 64 CAdds each adding a 48-lane
+// product into all 1,536 lanes, acc[j] += prod[j mod 48]).  Modular addition
+// is exact and associative, so the addends are summed at the operand's width,
+// S += prod (48 lanes), and the bundle is updated once, acc[j] += S[j mod 48],
+// before anything else touches it.  Every bundle any op reads is bit-identical
+// to the op-by-op order; the 64 full-width read-modify-writes (~160 GB each
+// way in total per op) become 64 narrow ones plus one wide one.
+bool Executor::wrap_deferrable(const hp::HeOp& op) const {
+  if (!o.wrap_defer || o.shard || o.dce || op.kind != hp::HeOpKind::kCAdd || !op.accumulate || op.ins.size() != 1)
+    return false;
+  const hp::LaneSlice& s = op.ins[0];
+  const u32 n = g.bundles[op.out.bundle].lanes, m = s.lane_count;
+  if (s.bundle == op.out.bundle || op.out.lane != 0 || op.out.lane_count != n || !m || m >= n || n % m) return false;
+  const Bundle* sh = shadow[op.out.bundle];
+  return !sh || (sh->lanes == m && shadow_level[op.out.bundle] == op.use_level);
+}
+
+void Executor::materialize(u32 b) {
+  Bundle* S = shadow[b];
+  shadow[b] = nullptr;
+  Bundle& X = get(b);
+  c.op_cadd(X, 0, g.bundles[b].lanes, *S, LaneMap{0, S->lanes}, nullptr, LaneMap{0, 1}, shadow_level[b], true);
+  c.free_bundle(S);
+  cur_comps[b] = 2;
+}
+
 void Executor::step(const hp::HeOp& op, int64_t i) {
   using K = hp::HeOpKind;
   const u32 L = op.use_level;
   if (op.kind == K::kEncode) return;  // weights are generated inside the PMult kernel (kGenerate)
+  for (const hp::LaneSlice& s : op.ins)
+    if (shadow[s.bundle]) materialize(s.bundle);
+  const bool defer = wrap_deferrable(op);
+  if (shadow[op.out.bundle] && !defer) materialize(op.out.bundle);
+  if (defer) {
+    const hp::LaneSlice& s = op.ins[0];
+    Bundle& in = input(s);
+    Bundle*& S = shadow[op.out.bundle];
+    if (!S) {
+      S = c.new_bundle(s.lane_count, 2, L, true);
+      shadow_level[op.out.bundle] = L;
+    }
+    c.op_cadd(*S, 0, s.lane_count, in, LaneMap{s.lane, s.lane_count}, nullptr, LaneMap{0, 1}, L, true);
+    get(op.out.bundle);  // the bundle exists from here on, as if written
+    cur_comps[op.out.bundle] = 2;
+    return;
+  }
   if (op.kind == K::kPAdd) throw Error(AEGIS_ELOGIC, "PAdd is not emitted by the reference lowering");
   if (op.kind == K::kPMult) {
     pmult(op);

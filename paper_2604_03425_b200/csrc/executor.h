@@ -27,6 +27,7 @@ struct RunOptions {
   void* reduce_user = nullptr;
   bool hoist = true;
   bool dce = false;  // skip output lanes no later op reads (final bundle unchanged)
+  bool wrap_defer = true;  // wrapped accumulating CAdds summed at the operand's width (bit-identical)
   std::vector<float>* op_ms = nullptr;  // if set: per-op device time (CUDA events)
 };
 
@@ -62,6 +63,8 @@ class Executor {
   void rot_run(const heplan::HeOp& op, int64_t i, u32 r0, u32 len);
   void reduce_partial(u32 bundle);
   void donate(const heplan::HeOp& op, int64_t i);
+  bool wrap_deferrable(const heplan::HeOp& op) const;
+  void materialize(u32 bundle);
   std::vector<std::pair<u32, u32>> out_runs(const heplan::HeOp& op) const;
   static LaneMap sub_map(const heplan::LaneSlice& s, u32 n, u32 pos, u32 len);
   u32 wrap_end(const heplan::HeOp& op, u32 pos, u32 end) const;
@@ -76,6 +79,8 @@ class Executor {
   std::vector<Group> groups;
   std::vector<int> group_of;
   std::vector<std::vector<char>> live;  // dce: [bundle][lane] read by a later op (or final)
+  std::vector<Bundle*> shadow;          // wrap_defer: pending sum S of a bundle's wrapped addends
+  std::vector<u32> shadow_level;
   u32 final_bundle = 0xffffffffu;
 };
 

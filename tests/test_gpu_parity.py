@@ -447,6 +447,24 @@ def test_dead_lane_elimination_keeps_final_bundle(logn, tokens, tmp_path):
     assert (h2 != h).any()
 
 
+@pytest.mark.parametrize("logn,tokens", [(12, 128)])  # score.acc: 96 lanes += 48-lane products
+def test_wrap_defer_bit_identical(logn, tokens):
+    """Wrapped accumulation (score.acc += prod[j mod m]) summed at the operand's
+    width and applied once: every bundle hash equals op-by-op execution, with
+    fewer kernel launches."""
+    c = ctx(logn)
+    g = c.graph(kind=0, tokens=tokens)
+    g.set_wrap_defer(False)
+    l0 = c.launch_count()
+    h = g.run(hashes=True)
+    l1 = c.launch_count()
+    g2 = c.graph(kind=0, tokens=tokens)
+    h2 = g2.run(hashes=True)
+    l2 = c.launch_count()
+    assert (h2 == h).all()
+    assert l2 - l1 < l1 - l0
+
+
 def _small_batch_ctx():
     """A production-size context whose operator workspaces hold 1-2 lanes, so
     every lane-batch loop (ModUp, key product / ModDown, rescale) iterates."""
