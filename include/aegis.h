@@ -81,6 +81,16 @@ int aegis_bundle_hash(aegis_ctx* ctx, const aegis_bundle* b, uint32_t comps, uin
 
 /* ---- keys (poly_ir.hpp:300-305: 0 = relin, 1000 + r = rotation r) -------- */
 int aegis_keys_generate(aegis_ctx* ctx, const uint64_t* key_ids, uint32_t count);
+/* caller-supplied key (replaces any key with this id): `words` =
+ * digits x 2 x (chain + 4) x N u64, layout [digit][comp][slot][N], canonical
+ * residues; slot s < chain is q_s, slot chain + i is the special prime P_i;
+ * digit j = the key for the centred lift of limbs [4j, 4j + 4).  coeff_domain
+ * != 0: rows are coefficient vectors (the library applies each slot's NTT),
+ * else NTT (evaluation) order.  Rotation keys (id 1000 + r) are given in the
+ * standard form for s(X^{5^r}) and stored pre-permuted internally.  The key
+ * for digit j must carry the CRT factor P * Qhat_j * [Qhat_j^{-1}]_{Q_j}
+ * (Qhat_j w.r.t. the full main chain), so one key serves every level. */
+int aegis_keys_upload(aegis_ctx* ctx, uint64_t key_id, const uint64_t* host, uint64_t words, int coeff_domain);
 int aegis_keys_bytes(const aegis_ctx* ctx, uint64_t* out);
 
 /* ---- polynomial instructions (PolyOpKind, poly_ir.hpp:23-32) -------------

@@ -51,6 +51,7 @@ SIGNATURES = [
     ("aegis_bundle_fill_input", ctypes.c_int, [vp, vp, u32]),
     ("aegis_bundle_hash", ctypes.c_int, [vp, vp, u32, u32, u64p]),
     ("aegis_keys_generate", ctypes.c_int, [vp, u64p, u32]),
+    ("aegis_keys_upload", ctypes.c_int, [vp, u64, u64p, u64, ctypes.c_int]),
     ("aegis_keys_bytes", ctypes.c_int, [vp, u64p]),
     ("aegis_ntt", ctypes.c_int, [vp, vp, u32, u32, u32, u32, ctypes.c_int]),
     ("aegis_automorphism", ctypes.c_int, [vp, vp, vp, u32, u32, u32, u64]),

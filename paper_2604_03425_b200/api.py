@@ -148,6 +148,17 @@ class Context:
         a = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
         self._call("aegis_keys_generate", _u64p(a), len(a))
 
+    def keys_upload(self, key_id, key, coeff_domain=True):
+        """Caller-supplied key, uint64 [digits][2][chain + 4][N] (include/aegis.h)."""
+        a = np.ascontiguousarray(key, dtype=np.uint64)
+        if a.shape != self.key_shape():
+            raise ValueError(f"key shape {a.shape} != {self.key_shape()}")
+        self._call("aegis_keys_upload", key_id, _u64p(a), a.size, 1 if coeff_domain else 0)
+
+    def key_shape(self):
+        """(digits, 2, chain + 4, N) of one key-switching key."""
+        return (-(-self.chain // 4), 2, self.chain + 4, 1 << self.log_n)
+
     # -- polynomial instructions --
     def ntt(self, b, lane=0, lanes=None, lo=0, hi=None, inverse=False):
         self._call("aegis_ntt", b.h, lane, b.lanes if lanes is None else lanes, lo,

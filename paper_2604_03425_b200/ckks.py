@@ -1,0 +1,211 @@
+"""Real CKKS encode / encrypt / decrypt and secret-derived key-switching keys
+around the GPU operators (first step).
+
+The reference idealises encryption away (graph inputs are "fresh
+activations", he_ir.hpp:178-188) and its keys are opaque.  This module turns the
+residue-exact GPU path into something that decrypts: a ternary secret s, keys
+in the hybrid form the library's key switch expects (include/aegis.h,
+aegis_keys_upload), the canonical-embedding encoder, and symmetric
+encryption.  Host-side NumPy + Python integers, meant for small rings
+(N <= 2^12) in tests and demos; the homomorphic operators themselves are the
+library's (Context.cmult / relin / rescale / rot).
+
+Conventions (all checked by tests/test_gpu_parity.py::test_ckks_*):
+  * slot j <-> evaluation at zeta^(5^j), zeta = exp(i pi / N); Rot by r (galois
+    5^r, rns_math.hpp:142-149) is a left rotation of the slot vector;
+  * a ciphertext (c0, c1) decrypts as c0 + c1 s; CMult gives (c0, c1, c2)
+    against (1, s, s^2); key-switching key digit j = (b_j, a_j) with
+    b_j = -a_j s + e_j + F_j s' (mod Q_L P), F_j = P Qhat_j [Qhat_j^-1]_{Q_j},
+    s' = s^2 (relin, id 0) or s(X^(5^r)) (rotation, id 1000 + r).
+"""
+import numpy as np
+
+SPECIAL_BASE = 60  # include/aegis_params.h AEGIS_MAX_MAIN_PRIMES: ext index of P_0
+ALPHA = 4          # AEGIS_SPECIAL_PRIMES: primes per key-switching digit
+
+
+def _shift(a, j, mods):
+    """X^j * a (negacyclic) for rows of residues a[k, N] mod mods[k]."""
+    n = a.shape[1]
+    r = np.empty_like(a)
+    r[:, j:] = a[:, :n - j]
+    r[:, :j] = (mods[:, None] - a[:, n - j:]) % mods[:, None]
+    return r
+
+
+def mul_small(a, t, mods):
+    """a * t mod (X^N + 1, mods) for a small-integer polynomial t (|t_i| < 2^16)."""
+    acc = np.zeros_like(a)
+    m = mods[:, None]
+    for j in np.nonzero(t)[0]:
+        c = int(t[j])
+        sh = _shift(a, int(j), mods)
+        if c < 0:
+            sh = (m - sh) % m
+            c = -c
+        acc = (acc + sh * np.uint64(c)) % m
+    return acc
+
+
+def negacyclic_int(a, b):
+    """Exact product of two small integer polynomials mod X^N + 1."""
+    n = len(a)
+    full = np.convolve(a.astype(np.int64), b.astype(np.int64))
+    out = full[:n].copy()
+    out[: len(full) - n] -= full[n:]
+    return out
+
+
+def automorphism_int(t, k):
+    """t(X^k) mod X^N + 1 for an integer polynomial t."""
+    n = len(t)
+    out = np.zeros_like(t)
+    for i in range(n):
+        e = (i * k) % (2 * n)
+        if e < n:
+            out[e] += t[i]
+        else:
+            out[e - n] -= t[i]
+    return out
+
+
+class Ckks:
+    """Secret key, key generation, encoder and symmetric encryption for `ctx`."""
+
+    def __init__(self, ctx, seed=1, hamming=64, sigma=3.2):
+        self.ctx = ctx
+        self.n = ctx.n
+        self.chain = ctx.chain
+        self.rng = np.random.default_rng(seed)
+        self.sigma = sigma
+        self.q = [int(ctx.prime(i)) for i in range(self.chain)]
+        self.p = [int(ctx.prime(SPECIAL_BASE + i)) for i in range(ALPHA)]
+        s = np.zeros(self.n, dtype=np.int64)
+        idx = self.rng.choice(self.n, size=min(hamming, self.n), replace=False)
+        s[idx] = self.rng.choice([-1, 1], size=len(idx))
+        self.s = s
+        # canonical embedding: slot j is the evaluation at zeta^(5^j)
+        m = self.n // 2
+        e = np.array([pow(5, j, 2 * self.n) for j in range(m)], dtype=np.int64)
+        self.roots = np.exp(1j * np.pi * e / self.n)
+        self.vander = self.roots[:, None] ** np.arange(self.n)[None, :]  # [slot][coeff]
+
+    # ---- encoding --------------------------------------------------------------
+    def encode(self, z, scale):
+        """Slot vector (N/2 complex) -> integer coefficients of round(scale * m)."""
+        z = np.asarray(z, dtype=np.complex128)
+        coef = (2.0 / self.n) * np.real(self.vander.conj().T @ z)
+        return np.rint(coef * scale).astype(object)
+
+    def decode(self, coef, scale):
+        """Integer (centred) coefficients -> slot vector / scale."""
+        c = np.array([float(x) for x in coef])
+        return (self.vander @ c) / scale
+
+    # ---- sampling --------------------------------------------------------------
+    def _error(self):
+        return np.rint(self.rng.normal(0.0, self.sigma, self.n)).astype(np.int64)
+
+    def _uniform(self, mods):
+        return np.stack([self.rng.integers(0, int(p), self.n, dtype=np.uint64) for p in mods])
+
+    @staticmethod
+    def _reduce_int(t, mods):
+        """Integer polynomial (python ints or int64) -> residues [k, N]."""
+        return np.stack([np.array([int(x) % int(p) for x in t], dtype=np.uint64) for p in mods])
+
+    # ---- keys ------------------------------------------------------------------
+    def key(self, s_prime):
+        """Hybrid key-switching key from s to s_prime, library layout (coefficient domain)."""
+        slots = self.q + self.p
+        mods = np.array(slots, dtype=np.uint64)
+        digits = -(-self.chain // ALPHA)
+        Q = 1
+        for x in self.q:
+            Q *= x
+        P = 1
+        for x in self.p:
+            P *= x
+        out = np.zeros((digits, 2, len(slots), self.n), dtype=np.uint64)
+        for j in range(digits):
+            Qj = 1
+            for x in self.q[ALPHA * j: ALPHA * (j + 1)]:
+                Qj *= x
+            qhat = Q // Qj
+            F = P * qhat * pow(qhat, -1, Qj)
+            a = self._uniform(slots)
+            e = self._reduce_int(self._error(), slots)
+            fs = self._scaled(s_prime, F, slots)
+            b = (mods[:, None] - mul_small(a, self.s, mods)) % mods[:, None]
+            b = (b + e) % mods[:, None]
+            b = (b + fs) % mods[:, None]
+            out[j, 0], out[j, 1] = b, a
+        return out
+
+    @staticmethod
+    def _scaled(t, F, mods):
+        """(F * t) mod each modulus, t a small-integer polynomial, exact."""
+        rows = []
+        for m in mods:
+            f = F % m
+            rows.append(np.array([(f * int(x)) % m for x in t], dtype=np.uint64))
+        return np.stack(rows)
+
+    def upload_relin_key(self):
+        self.ctx.keys_upload(0, self.key(negacyclic_int(self.s, self.s)))
+
+    def upload_rotation_key(self, r):
+        k = pow(5, r % self.n, 2 * self.n)
+        self.ctx.keys_upload(1000 + r, self.key(automorphism_int(self.s, k)))
+
+    # ---- encryption ------------------------------------------------------------
+    def encrypt(self, z, scale, level, bundle=None, lane=0):
+        """Symmetric encryption of slot vector z at `level` into lane `lane` of a
+        (new) 2-component bundle, NTT (evaluation) domain as the library keeps it."""
+        mods = np.array(self.q[:level], dtype=np.uint64)
+        m = self._reduce_int(self.encode(z, scale), self.q[:level])
+        a = self._uniform(self.q[:level])
+        e = self._reduce_int(self._error(), self.q[:level])
+        c0 = (mods[:, None] - mul_small(a, self.s, mods)) % mods[:, None]
+        c0 = (c0 + e + m) % mods[:, None]
+        if bundle is None:
+            bundle = self.ctx.bundle(1, 2, level)
+        host = bundle.download()
+        host[lane, 0, :level], host[lane, 1, :level] = c0, a
+        bundle.upload(host)
+        self.ctx.ntt(bundle, lane=lane, lanes=1, lo=0, hi=level - 1)
+        return bundle
+
+    def decrypt(self, bundle, scale, level, lane=0):
+        """Slot vector of lane `lane` (first two components, `level` limbs)."""
+        tmp = self.ctx.bundle(1, bundle.comps, bundle.level)
+        host = bundle.download()
+        tmp.upload(host[lane: lane + 1])
+        self.ctx.ntt(tmp, lanes=1, lo=0, hi=level - 1, inverse=True)
+        h = tmp.download()
+        tmp.free()
+        mods = np.array(self.q[:level], dtype=np.uint64)
+        c0 = h[0, 0, :level] % mods[:, None]
+        c1 = h[0, 1, :level] % mods[:, None]
+        x = (c0 + mul_small(c1, self.s, mods)) % mods[:, None]
+        return self.decode(self.crt(x, level), scale)
+
+    def crt(self, x, level):
+        """Residues [level, N] -> centred integers."""
+        q = self.q[:level]
+        Q = 1
+        for v in q:
+            Q *= v
+        terms = []
+        for i, v in enumerate(q):
+            qh = Q // v
+            terms.append((qh, pow(qh % v, -1, v)))
+        out = []
+        for t in range(self.n):
+            acc = 0
+            for i, v in enumerate(q):
+                qh, inv = terms[i]
+                acc += (int(x[i, t]) * inv % v) * qh
+            acc %= Q
+            out.append(acc - Q if acc > Q // 2 else acc)
+        return out

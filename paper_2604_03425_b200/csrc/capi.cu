@@ -241,6 +241,12 @@ int aegis_keys_generate(aegis_ctx* ctx, const uint64_t* ids, uint32_t count) {
     for (uint32_t i = 0; i < count; ++i) ctx->c->generate_key(ids[i]);
   });
 }
+int aegis_keys_upload(aegis_ctx* ctx, uint64_t key_id, const uint64_t* host, uint64_t words, int coeff_domain) {
+  return guard(ctx, [&] {
+    if (!host) throw Error(AEGIS_EINVAL, "key upload: null host buffer");
+    ctx->c->upload_key(key_id, reinterpret_cast<const aegis::u64*>(host), words, coeff_domain != 0);
+  });
+}
 int aegis_keys_bytes(const aegis_ctx* ctx, uint64_t* out) {
   if (!ctx || !out) return AEGIS_EINVAL;
   *out = ctx->c->total_key_bytes();

@@ -354,10 +354,9 @@ const Plan& Context::plan(const std::vector<u32>& src, const std::vector<u32>& d
   return plans_.emplace(key, pl).first->second;
 }
 
-void Context::generate_key(u64 key_id) {
-  if (keys_.count(key_id)) return;
+u64* Context::alloc_key() {
   u64* k = nullptr;
-  const size_t words = (size_t)key_digits() * 2 * key_slots() * n;
+  const size_t words = key_bytes() / 8;
   cudaError_t e = cudaMalloc(&k, words * 8);
   if (e != cudaSuccess) {  // idle arena / pool memory may hold the space: release it and retry
     cudaGetLastError();
@@ -368,25 +367,64 @@ void Context::generate_key(u64 key_id) {
     cudaGetLastError();
     throw Error(AEGIS_EOOM, "key allocation failed");
   }
+  return k;
+}
+
+// Rotation key for offset r = key_id - 1000 is stored pre-permuted by the
+// inverse automorphism: key'_r = auto_{k^-1}(key_r).  Then
+//   KS(auto_k(c1)) = auto_k(ModDown(sum_j ModUp(c1)_j * key'_j))
+// exactly (auto_k is a signed coefficient permutation; the centred lift and
+// the rounding division commute with it), so the ModUp of c1 no longer
+// depends on the offset and can be hoisted across rotations.
+void Context::prepermute_key(u64 key_id, u64* k) {
+  if (key_id < 500) return;
+  const size_t words = key_bytes() / 8;
+  const u64 gk = galois_of((int)((long long)key_id - 1000));
+  const u64 ginv = h_powmod(gk, (u64)n - 1, 2ull * n);  // k^-1 mod 2N (the group has order N)
+  u64* tmp = alloc(words);
+  const u32 rows = key_digits() * 2 * key_slots();
+  AEGIS_CHECK_CUDA(launch_automorphism(View{tmp, rows, 1, 1}, LaneMap{0, rows}, View{k, rows, 1, 1},
+                                       LaneMap{0, rows}, rows, 1, 1, log_n, ginv, stream));
+  count();
+  AEGIS_CHECK_CUDA(cudaMemcpyAsync(k, tmp, words * 8, cudaMemcpyDeviceToDevice, stream));
+  release(tmp);
+}
+
+void Context::generate_key(u64 key_id) {
+  if (keys_.count(key_id)) return;
+  u64* k = alloc_key();
   AEGIS_CHECK_CUDA(launch_fill_key(k, key_digits(), key_slots(), n, seed_key, key_id, d_key_slot_ext_, d_pc, stream));
   count();
-  if (key_id >= 500) {
-    // Rotation key for offset r = key_id - 1000 is stored pre-permuted by the
-    // inverse automorphism: key'_r = auto_{k^-1}(key_r).  Then
-    //   KS(auto_k(c1)) = auto_k(ModDown(sum_j ModUp(c1)_j * key'_j))
-    // exactly (auto_k is a signed coefficient permutation; the centred lift and
-    // the rounding division commute with it), so the ModUp of c1 no longer
-    // depends on the offset and can be hoisted across rotations.
-    const u64 gk = galois_of((int)((long long)key_id - 1000));
-    const u64 ginv = h_powmod(gk, (u64)n - 1, 2ull * n);  // k^-1 mod 2N (the group has order N)
-    u64* tmp = alloc(words);
-    const u32 rows = key_digits() * 2 * key_slots();
-    AEGIS_CHECK_CUDA(launch_automorphism(View{tmp, rows, 1, 1}, LaneMap{0, rows}, View{k, rows, 1, 1},
-                                         LaneMap{0, rows}, rows, 1, 1, log_n, ginv, stream));
-    count();
-    AEGIS_CHECK_CUDA(cudaMemcpyAsync(k, tmp, words * 8, cudaMemcpyDeviceToDevice, stream));
-    release(tmp);
+  prepermute_key(key_id, k);
+  keys_[key_id] = k;
+}
+
+// Caller-supplied key (SURVEY §8(b) aegis_keys_upload): [digit][comp][slot][N]
+// canonical residues, slot s < chain -> q_s, else P_{s - chain}.  Digit j holds
+// the key for the lift of limbs [4j, 4j+4) (key_switch, poly_ir.hpp:219-298,
+// hybrid form).  Rotation keys are given in the standard (unpermuted) form.
+void Context::upload_key(u64 key_id, const u64* host, size_t words, bool coeff_domain) {
+  if (words != key_bytes() / 8)
+    throw Error(AEGIS_EINVAL, "key upload: expected " + std::to_string(key_bytes() / 8) + " words, got " +
+                                  std::to_string(words));
+  auto it = keys_.find(key_id);
+  if (it != keys_.end()) {
+    AEGIS_CHECK_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(it->second);
+    keys_.erase(it);
   }
+  u64* k = alloc_key();
+  AEGIS_CHECK_CUDA(cudaMemcpyAsync(k, host, words * 8, cudaMemcpyHostToDevice, stream));
+  if (coeff_domain) {
+    std::vector<u32> off(key_slots()), pr(key_slots());
+    for (u32 s = 0; s < key_slots(); ++s) {
+      off[s] = s;
+      pr[s] = s < chain ? s : kSpecialBase + (s - chain);
+    }
+    ntt(k, (size_t)key_slots() * n, key_digits() * 2, off, pr, false);
+  }
+  prepermute_key(key_id, k);
+  AEGIS_CHECK_CUDA(cudaStreamSynchronize(stream));  // the host buffer may be pageable / reused
   keys_[key_id] = k;
 }
 

@@ -77,6 +77,7 @@ class Context {
 
   // keys
   void generate_key(u64 key_id);
+  void upload_key(u64 key_id, const u64* host, size_t words, bool coeff_domain);
   const u64* key(u64 key_id);
   u32 key_slots() const { return chain + kAlpha; }
   u32 key_digits() const { return (chain + kAlpha - 1) / kAlpha; }
@@ -162,6 +163,8 @@ class Context {
   std::map<std::vector<u32>, Plan> plans_;
   std::map<u64, u64*> keys_;
   u32* d_key_slot_ext_ = nullptr;  // key slot -> ext prime
+  u64* alloc_key();
+  void prepermute_key(u64 key_id, u64* k);
   cudaMemPool_t pool_ = nullptr;
   std::unique_ptr<Arena> arena_;
 };

@@ -521,3 +521,36 @@ def test_multibatch_hoisted_rotations_production(tmp_path):
     h_gpu = g.run(hashes=True)
     h_cpu = orc(16).run_graph(path)
     assert (h_gpu[: len(h_cpu)] == h_cpu).all()
+
+
+@pytest.mark.parametrize("level", [17, 35])
+def test_ckks_real_keys_decrypt(level):
+    """SURVEY §8(f) rank 3, first step: with a ternary secret, keys from
+    aegis_keys_upload and real symmetric encryption (paper_2604_03425_b200.ckks),
+    the GPU operators are correct CKKS operations -- CMult+Relin+Rescale decrypts
+    to z^2 and Rot by r to the left-rotated slots (tolerances in the asserts)."""
+    from paper_2604_03425_b200 import Context
+    from paper_2604_03425_b200.ckks import Ckks
+    c = Context(log_n=11)  # private context: uploaded keys must not leak into other tests
+    try:
+        k = Ckks(c, seed=7)
+        rng = np.random.default_rng(level)
+        z = rng.uniform(-1, 1, c.n // 2) + 1j * rng.uniform(-1, 1, c.n // 2)
+        scale = 2.0 ** 40
+        ct = k.encrypt(z, scale, level)
+        assert np.abs(k.decrypt(ct, scale, level) - z).max() < 1e-7
+        k.upload_relin_key()
+        sq = c.bundle(1, 3, level)
+        c.cmult(sq, ct, ct, level)
+        c.relin(sq, level)
+        out = c.bundle(1, 2, level - 1)
+        c.rescale(out, sq, level)
+        s2 = scale * scale / k.q[level - 1]
+        assert np.abs(k.decrypt(out, s2, level - 1) - z * z).max() < 1e-6
+        for r in (1, 7, -3):
+            k.upload_rotation_key(r)
+            o = c.bundle(1, 2, level)
+            c.rot(o, ct, r, level)
+            assert np.abs(k.decrypt(o, scale, level) - np.roll(z, -r)).max() < 1e-7
+    finally:
+        c.close()
