@@ -59,13 +59,11 @@ def negacyclic_int(a, b):
 def automorphism_int(t, k):
     """t(X^k) mod X^N + 1 for an integer polynomial t."""
     n = len(t)
+    e = (np.arange(n, dtype=np.int64) * k) % (2 * n)
     out = np.zeros_like(t)
-    for i in range(n):
-        e = (i * k) % (2 * n)
-        if e < n:
-            out[e] += t[i]
-        else:
-            out[e - n] -= t[i]
+    lo = e < n
+    out[e[lo]] = t[lo]
+    out[e[~lo] - n] = -t[~lo]
     return out
 
 
@@ -84,23 +82,32 @@ class Ckks:
         idx = self.rng.choice(self.n, size=min(hamming, self.n), replace=False)
         s[idx] = self.rng.choice([-1, 1], size=len(idx))
         self.s = s
-        # canonical embedding: slot j is the evaluation at zeta^(5^j)
-        m = self.n // 2
-        e = np.array([pow(5, j, 2 * self.n) for j in range(m)], dtype=np.int64)
-        self.roots = np.exp(1j * np.pi * e / self.n)
-        self.vander = self.roots[:, None] ** np.arange(self.n)[None, :]  # [slot][coeff]
+        # canonical embedding: slot j is the evaluation at zeta^(5^j), zeta =
+        # exp(i pi / N).  m(zeta^(2t+1)) = sum_k (m_k zeta^k) w^(tk), w = zeta^2,
+        # is one N-point DFT, so encode / decode are O(N log N) at any N
+        n, m = self.n, self.n // 2
+        g = np.ones(m, dtype=np.int64)
+        for j in range(1, m):
+            g[j] = g[j - 1] * 5 % (2 * n)
+        self.slot_t = (g - 1) // 2                  # 2t + 1 = 5^j
+        self.conj_t = (2 * n - g - 1) // 2          # the conjugate root
+        self.twist = np.exp(1j * np.pi * np.arange(n) / n)  # zeta^k
 
     # ---- encoding --------------------------------------------------------------
     def encode(self, z, scale):
-        """Slot vector (N/2 complex) -> integer coefficients of round(scale * m)."""
+        """Slot vector (N/2 complex) -> int64 coefficients of round(scale * m)."""
         z = np.asarray(z, dtype=np.complex128)
-        coef = (2.0 / self.n) * np.real(self.vander.conj().T @ z)
-        return np.rint(coef * scale).astype(object)
+        v = np.zeros(self.n, dtype=np.complex128)
+        v[self.slot_t] = z
+        v[self.conj_t] = np.conj(z)
+        coef = np.real(np.fft.fft(v) / self.n / self.twist)  # m_k = zeta^-k (1/N) sum_t v_t w^-tk
+        return np.rint(coef * scale).astype(np.int64)
 
     def decode(self, coef, scale):
         """Integer (centred) coefficients -> slot vector / scale."""
         c = np.array([float(x) for x in coef])
-        return (self.vander @ c) / scale
+        v = np.fft.ifft(c * self.twist) * self.n
+        return v[self.slot_t] / scale
 
     # ---- sampling --------------------------------------------------------------
     def _error(self):
@@ -111,8 +118,9 @@ class Ckks:
 
     @staticmethod
     def _reduce_int(t, mods):
-        """Integer polynomial (python ints or int64) -> residues [k, N]."""
-        return np.stack([np.array([int(x) % int(p) for x in t], dtype=np.uint64) for p in mods])
+        """Small integer polynomial (int64, |t| < 2^62) -> residues [k, N]."""
+        t = np.asarray(t, dtype=np.int64)
+        return np.stack([(t % np.int64(p)).astype(np.uint64) for p in mods])
 
     # ---- keys ------------------------------------------------------------------
     def key(self, s_prime):
@@ -144,12 +152,11 @@ class Ckks:
 
     @staticmethod
     def _scaled(t, F, mods):
-        """(F * t) mod each modulus, t a small-integer polynomial, exact."""
-        rows = []
-        for m in mods:
-            f = F % m
-            rows.append(np.array([(f * int(x)) % m for x in t], dtype=np.uint64))
-        return np.stack(rows)
+        """(F * t) mod each modulus for a small-integer polynomial t (|t| < 2^16), exact."""
+        t = np.asarray(t, dtype=np.int64)
+        if np.abs(t).max(initial=0) >= 1 << 16:
+            raise ValueError("_scaled: coefficients too large")
+        return np.stack([((np.int64(F % m) * t) % np.int64(m)).astype(np.uint64) for m in mods])
 
     def upload_relin_key(self):
         self.ctx.keys_upload(0, self.key(negacyclic_int(self.s, self.s)))
@@ -191,21 +198,15 @@ class Ckks:
         return self.decode(self.crt(x, level), scale)
 
     def crt(self, x, level):
-        """Residues [level, N] -> centred integers."""
+        """Residues [level, N] -> centred integers (Python ints, object array)."""
         q = self.q[:level]
         Q = 1
         for v in q:
             Q *= v
-        terms = []
+        acc = np.zeros(self.n, dtype=object)
         for i, v in enumerate(q):
             qh = Q // v
-            terms.append((qh, pow(qh % v, -1, v)))
-        out = []
-        for t in range(self.n):
-            acc = 0
-            for i, v in enumerate(q):
-                qh, inv = terms[i]
-                acc += (int(x[i, t]) * inv % v) * qh
-            acc %= Q
-            out.append(acc - Q if acc > Q // 2 else acc)
-        return out
+            inv = pow(qh % v, -1, v)
+            acc = acc + (x[i].astype(object) * inv % v) * qh
+        acc = acc % Q
+        return np.where(acc > Q // 2, acc - Q, acc)

@@ -3,7 +3,7 @@ secret, keys via aegis_keys_upload, symmetric encryption, then CMult + Relin +
 Rescale, Rot and a 4-step rotate-and-sum; prints max |decrypted - expected|.
 Dev tool; GPU.
 
-    python tools/ckks_demo.py [--log-n 12] [--levels 5,17,35]
+    python tools/ckks_demo.py [--log-n 16] [--levels 5,17,35]
 """
 import argparse
 import os
@@ -20,7 +20,7 @@ from paper_2604_03425_b200.ckks import Ckks  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--log-n", type=int, default=12)
+    ap.add_argument("--log-n", type=int, default=16)
     ap.add_argument("--levels", default="5,17,35")
     ap.add_argument("--scale-bits", type=int, default=40)
     a = ap.parse_args()
