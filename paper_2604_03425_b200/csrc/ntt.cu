@@ -506,12 +506,15 @@ __device__ __forceinline__ void load_w_blob(double (&w)[15], const double* sp) {
     for (int q = 0; q < (1 << sg); ++q) w[(1 << sg) - 1 + q] = sp[((1 << sg) - 1 + q) * 17];
 }
 // pass-B round-1 twiddles of one sub from the blob (half-warp broadcast)
-__device__ __forceinline__ void load_w_blob1(double (&w)[15], const double* sb) {
+[[maybe_unused]] __device__ __forceinline__ void load_w_blob1(double (&w)[15], const double* sb) {
 #pragma unroll
   for (int i = 0; i < 15; ++i) w[i] = sb[kTw1 + i];
 }
+// 0: round-1 twiddles from the w-only table, so the blob's TMA copy is only
+// waited for before round 2 (measured 0.4-0.6 % faster key switches at the
+// end of round 1; the blob wait was 12 % of fwd_b_fin's stall samples)
 #ifndef AEGIS_BLOB_R1
-#define AEGIS_BLOB_R1 1
+#define AEGIS_BLOB_R1 0
 #endif
 struct WArr {
   const double* w;
