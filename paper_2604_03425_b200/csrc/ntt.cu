@@ -658,7 +658,10 @@ __device__ __forceinline__ void tile_cfwd_a(const NttLaunch& L, const NttConvIn&
     for (int t = 0; t < T; ++t) {
       Acc3 a;
 #pragma unroll
-      for (int i = 0; i <= K; ++i) mac24(a, Split{w[i].x, w[i].y}, hs[t][i]);
+      for (int i = 0; i < K; ++i) mac24(a, Split{w[i].x, w[i].y}, hs[t][i]);
+      // the overflow count v <= k has a zero high limb: two products, not four
+      a.c0 += (u64)w[K].x * hs[t][K].lo;
+      a.c1 += (u64)w[K].x * hs[t][K].hi;
       // q = floor((S >> 32) floor(2^96/d) / 2^64) is within 3 below S/d: r = S - q d in [0, 3d)
       const u64 top = (a.c2 << 16) + (a.c1 >> 8) + (a.c0 >> 32);
       const u64 q = __umul64hi(top, mu[t]);
