@@ -215,11 +215,12 @@ def run_aegis(args):
     g = c.graph(kind=0, tokens=args.tokens, layers=args.layers)
     tg_total = -(-args.tokens // ((1 << N_LOG) // 2 // 64))
     if ws > 1:
-        from paper_2604_03425_b200.dist import make_reducer, token_group_comms
+        from paper_2604_03425_b200.dist import P2pReducer, make_reducer, token_group_comms
         g.set_shard(ws, rank)
         groups, m = token_group_comms(ws, tg_total)
-        if m > 1:
-            g.set_reducer(make_reducer(groups, rank % m))
+        if m > 1:  # PCMM reduce-scatter over peer memory (AEGIS_REDUCER=nccl: the NCCL collective)
+            nccl = os.environ.get("AEGIS_REDUCER", "p2p") == "nccl"
+            g.set_reducer(make_reducer(groups, rank % m) if nccl else P2pReducer(c, groups, rank % m))
     c.keys_generate(g.key_ids())
     c.sync()
     st = torch.cuda.ExternalStream(c.stream)

@@ -37,6 +37,7 @@ extern "C" {
 typedef struct aegis_ctx aegis_ctx;
 typedef struct aegis_bundle aegis_bundle;
 typedef struct aegis_graph aegis_graph;
+typedef struct aegis_p2p aegis_p2p;
 
 /* CkksProfile (ckks.hpp:21-46) plus the seeds of the synthetic workload. */
 typedef struct aegis_params {
@@ -161,6 +162,19 @@ int aegis_graph_set_shard(aegis_graph* g, uint32_t world, uint32_t rank);
  * rank's share at buf + part*words_per_rank; return 0 on success. */
 typedef int (*aegis_reduce_fn)(void* user, uint64_t* buf, uint64_t words_per_rank, uint32_t group);
 int aegis_graph_set_reducer(aegis_graph* g, aegis_reduce_fn fn, void* user);
+/* The same reduce-scatter over CUDA IPC / NVLink peer memory instead of a
+ * library collective (csrc/p2p.cu; replaces the comm stream's kReduceOutputs
+ * event, comm_plan.hpp:127, 238).  Each rank of a token group creates a window
+ * (bytes >= m * words_per_rank * 8) and exports its 64-byte IPC handle; after the
+ * handles are exchanged, open maps all m of them.  Per reduction the host runs
+ * stage(buf, m * words) -> group barrier -> reduce(buf + part * words, words,
+ * part) -> group barrier.  reduce writes the uint64 sum of the m windows'
+ * share `part` (the reduce hook's semantics). */
+int aegis_p2p_create(aegis_ctx* ctx, uint64_t bytes, void* handle_out, aegis_p2p** out);
+int aegis_p2p_open(aegis_ctx* ctx, aegis_p2p* w, const void* handles, uint32_t m, uint32_t self);
+int aegis_p2p_stage(aegis_ctx* ctx, aegis_p2p* w, const uint64_t* buf, uint64_t words);
+int aegis_p2p_reduce(aegis_ctx* ctx, aegis_p2p* w, uint64_t* dst, uint64_t words_per_rank, uint32_t part);
+int aegis_p2p_destroy(aegis_p2p* w);
 /* lane ownership of bundle `bundle` under the current shard (1 = owned) */
 int aegis_graph_owned_lanes(const aegis_graph* g, uint32_t bundle, uint8_t* mask, uint32_t cap);
 int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* tg_lo, uint32_t* tg_hi,

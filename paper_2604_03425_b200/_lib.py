@@ -87,6 +87,11 @@ SIGNATURES = [
     ("aegis_graph_key_ids", ctypes.c_int, [vp, u64p, u32, u32p]),
     ("aegis_graph_free", ctypes.c_int, [vp]),
     ("aegis_graph_peak_bytes", u64, [vp]),
+    ("aegis_p2p_create", ctypes.c_int, [vp, u64, vp, ctypes.POINTER(vp)]),
+    ("aegis_p2p_open", ctypes.c_int, [vp, vp, vp, u32, u32]),
+    ("aegis_p2p_stage", ctypes.c_int, [vp, vp, vp, u64]),
+    ("aegis_p2p_reduce", ctypes.c_int, [vp, vp, vp, u64, u32]),
+    ("aegis_p2p_destroy", ctypes.c_int, [vp]),
 ]
 
 # int (*)(void* user, uint64_t* buf, uint64_t words_per_rank, uint32_t group)

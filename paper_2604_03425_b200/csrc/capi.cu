@@ -11,6 +11,7 @@
 
 #include "context.h"
 #include "executor.h"
+#include "p2p.h"
 #include "heplan_ir.h"
 
 using aegis::Bundle;
@@ -687,5 +688,40 @@ int aegis_graph_free(aegis_graph* g) {
   return AEGIS_OK;
 }
 uint64_t aegis_graph_peak_bytes(const aegis_graph* g) { return g ? g->peak : 0; }
+
+
+struct aegis_p2p {
+  std::unique_ptr<aegis::P2pWindow> w;
+};
+
+int aegis_p2p_create(aegis_ctx* ctx, uint64_t bytes, void* handle_out, aegis_p2p** out) {
+  if (!ctx || !handle_out || !out) return AEGIS_EINVAL;
+  return guard(ctx, [&] {
+    auto* h = new aegis_p2p;
+    try {
+      h->w.reset(aegis::p2p_create(*ctx->c, bytes, handle_out));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+int aegis_p2p_open(aegis_ctx* ctx, aegis_p2p* w, const void* handles, uint32_t m, uint32_t self) {
+  if (!ctx || !w || !handles) return AEGIS_EINVAL;
+  return guard(ctx, [&] { aegis::p2p_open(*w->w, handles, m, self); });
+}
+int aegis_p2p_stage(aegis_ctx* ctx, aegis_p2p* w, const uint64_t* buf, uint64_t words) {
+  if (!ctx || !w || !buf) return AEGIS_EINVAL;
+  return guard(ctx, [&] { aegis::p2p_stage(*ctx->c, *w->w, reinterpret_cast<const aegis::u64*>(buf), words); });
+}
+int aegis_p2p_reduce(aegis_ctx* ctx, aegis_p2p* w, uint64_t* dst, uint64_t words_per_rank, uint32_t part) {
+  if (!ctx || !w || !dst) return AEGIS_EINVAL;
+  return guard(ctx, [&] { aegis::p2p_reduce(*ctx->c, *w->w, reinterpret_cast<aegis::u64*>(dst), words_per_rank, part); });
+}
+int aegis_p2p_destroy(aegis_p2p* w) {
+  delete w;
+  return AEGIS_OK;
+}
 
 }  // extern "C"

@@ -112,6 +112,30 @@ ShardPlan make_shard_plan(const heplan::HeOpGraph& g, uint32_t tg_total, uint32_
   for (size_t b = 0; b < g.bundles.size(); ++b)
     for (const LaneTag& t : P.tags[b])
       if (t.pos >= 0 && (uint32_t)t.pos + 1 > P.npos[b]) P.npos[b] = (uint32_t)t.pos + 1;
+  if (P.m > 1) {
+    // A token group split over m ranks is only exact if every lane-local op
+    // reads operand lanes owned by the same part as its output lane (PCMM is
+    // input-stationary and exempt: its reduce-scatter moves the data).  Shapes
+    // whose operands wrap onto fewer positions than the output (e.g. score
+    // lanes < output lanes at very small T / N) would read lanes no rank of
+    // this part computed: refuse them instead of computing garbage.
+    for (const heplan::HeOp& op : g.ops) {
+      if (op.kind == K::kEncode || op.kind == K::kPMult) continue;
+      const uint32_t n = op.out.lane_count;
+      for (uint32_t l = 0; l < n; ++l) {
+        const LaneTag ot = P.tags[op.out.bundle][op.out.lane + l];
+        const uint32_t want = P.part_of(op.out.bundle, ot.pos);
+        for (const heplan::LaneSlice& a : op.ins) {
+          const uint32_t il = a.lane + (a.lane_count == n ? l : l % a.lane_count);
+          if (P.part_of(a.bundle, P.tags[a.bundle][il].pos) != want)
+            throw std::invalid_argument("token group split over " + std::to_string(P.m) + " ranks: op " +
+                                        std::to_string(op.id) + " (" + g.bundles[op.out.bundle].tag +
+                                        ") reads lanes another rank owns; use world <= token groups (" +
+                                        std::to_string(tg_total) + ") for this shape");
+        }
+      }
+    }
+  }
   return P;
 }
 

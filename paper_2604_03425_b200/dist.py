@@ -7,6 +7,8 @@ partial sums for all of the group's output lanes; one reduce-scatter (uint64
 sum -- residues < 2^46, so m * p never wraps) leaves each rank the complete
 sums for the lanes it owns, which libaegis then reduces mod p.
 """
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -56,3 +58,67 @@ def make_reducer(groups, part):
         reduce_scatter_words(full, part, g)
         torch.cuda.current_stream().synchronize()
     return fn
+
+
+class P2pReducer:
+    """The reduce hook over CUDA IPC / NVLink peer memory (csrc/p2p.cu) instead of
+    an NCCL collective: every rank of a token group exposes a staging window,
+    and each rank's kernel sums its share directly out of the m windows.
+    Windows are created lazily at the first reduction of a group (all m ranks
+    reach it together) and grown collectively when a larger one is needed."""
+
+    def __init__(self, ctx, groups, part):
+        self.ctx, self.groups, self.part = ctx, groups, part
+        self.win = {}  # token group -> (handle, bytes)
+        self.fallback = None  # NCCL reducer if any rank of the group cannot map the windows
+
+    def _window(self, group, nbytes):
+        w = self.win.get(group)
+        if w is not None and w[1] >= nbytes:
+            return w[0]
+        lib = self.ctx.lib
+        if w is not None:
+            lib.aegis_p2p_destroy(w[0])
+        g = self.groups[group]
+        raw = (ctypes.c_char * 64)()
+        h = ctypes.c_void_p()
+        self.ctx._call("aegis_p2p_create", nbytes, ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(h))
+        m = dist.get_world_size(g)
+        handles = [None] * m
+        dist.all_gather_object(handles, bytes(raw), group=g)
+        allh = ctypes.create_string_buffer(b"".join(handles), 64 * m)
+        err = ""
+        try:
+            self.ctx._call("aegis_p2p_open", h, ctypes.cast(allh, ctypes.c_void_p), m, self.part)
+        except Exception as e:  # noqa: BLE001 -- decided collectively below
+            err = repr(e)
+        errs = [None] * m
+        dist.all_gather_object(errs, err, group=g)
+        if any(errs):
+            import sys
+            print(f"aegis: peer-memory windows unavailable ({next(e for e in errs if e)}); "
+                  "using the NCCL reduce-scatter", file=sys.stderr)
+            lib.aegis_p2p_destroy(h)
+            self.fallback = make_reducer(self.groups, self.part)
+            return None
+        self.win[group] = (h, nbytes)
+        return h
+
+    def __call__(self, buf_ptr, words_per_rank, group):
+        if self.fallback:
+            return self.fallback(buf_ptr, words_per_rank, group)
+        g = self.groups[group]
+        m = dist.get_world_size(g)
+        h = self._window(group, words_per_rank * m * 8)
+        if h is None:
+            return self.fallback(buf_ptr, words_per_rank, group)
+        self.ctx._call("aegis_p2p_stage", h, ctypes.c_void_p(buf_ptr), words_per_rank * m)
+        dist.barrier(group=g)  # every window holds its rank's partial sums
+        self.ctx._call("aegis_p2p_reduce", h, ctypes.c_void_p(buf_ptr + self.part * words_per_rank * 8),
+                       words_per_rank, self.part)
+        dist.barrier(group=g)  # nobody restages before every peer has read
+
+    def close(self):
+        for h, _ in self.win.values():
+            self.ctx.lib.aegis_p2p_destroy(h)
+        self.win = {}

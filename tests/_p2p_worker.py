@@ -1,0 +1,51 @@
+"""torchrun worker for tests/test_gpu_p2p.py: token-group shards whose PCMM
+reduce-scatter runs over CUDA IPC peer memory (dist.P2pReducer, csrc/p2p.cu).
+All ranks share GPU 0 (same-device IPC); rank 0 checks that the per-rank
+bundle hashes sum to the unsharded run's and prints P2P_OK."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2604_03425_b200 import Context  # noqa: E402
+from paper_2604_03425_b200.dist import P2pReducer, make_reducer, token_group_comms  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, ws = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    tokens = int(os.environ.get("P2P_TOKENS", "64"))
+    c = Context(log_n=11)
+    g = c.graph(kind=0, tokens=tokens)
+    g.set_shard(ws, rank)
+    info = g.shard_info()
+    groups, m = token_group_comms(ws, info["tg_total"])
+    red = P2pReducer(c, groups, rank % m)
+    if os.environ.get("P2P_REDUCER") == "collective":  # the torch.distributed path, for comparison
+        red.fallback = make_reducer(groups, rank % m)
+    g.set_reducer(red)
+    h = g.run(hashes=True)
+    hs = [None] * ws
+    dist.all_gather_object(hs, h.tolist())
+    used = red.fallback is None and len(red.win) > 0
+    if rank == 0:
+        base = c.graph(kind=0, tokens=tokens).run(hashes=True)
+        total = np.zeros_like(base)
+        for x in hs:
+            total = total + np.array(x, dtype=np.uint64)
+        bad = int((total != base).sum())
+        print(f"P2P_{'OK' if bad == 0 else 'MISMATCH'} bundles={len(base)} bad={bad} m={m} used_p2p={used}",
+              flush=True)
+    red.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

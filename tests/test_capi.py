@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "aegis.h")
 def declared():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(aegis_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(aegis_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -1,0 +1,34 @@
+"""PCMM reduce-scatter over CUDA IPC / NVLink peer memory (csrc/p2p.cu,
+dist.P2pReducer) in real separate processes on one GPU (same-device IPC):
+N = 2^11, T = 64 has 4 token groups (the T = 2048, N = 2^16 structure), so
+world 8 / 16 puts 2 / 4 ranks on each group.  Bundle hashes summed over the
+ranks must equal the unsharded run, with the peer-memory path actually used."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,tokens", [(8, 64), (16, 64)])
+def test_p2p_reduce_scatter_processes(world, tokens):
+    env = dict(os.environ, P2P_TOKENS=str(tokens))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "_p2p_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("P2P_")]
+    assert line and line[0].startswith("P2P_OK") and "used_p2p=True" in line[0], r.stdout[-2000:] + r.stderr[-2000:]

@@ -154,3 +154,17 @@ def test_two_rank_gloo_partition():
     for rank, overlaps, owned_total, ok_rs in res:
         assert overlaps == 0 and ok_rs
     assert res[0][2] == res[1][2] > 0
+
+
+def test_split_token_group_refuses_wrapping_shapes():
+    """A token group split over m > 1 ranks is exact only when every lane-local
+    op reads lanes of its own part; at very small T the score accumulator wraps
+    onto fewer lanes than its consumers, so the plan must refuse (not compute
+    garbage), while the production shape (T = 2048, 8 ranks) is accepted."""
+    from paper_2604_03425_b200.api import plan_graph
+    g = plan_graph(log_n=11, tokens=16)
+    with pytest.raises(ValueError, match="token group split"):
+        g.set_shard(2, 0)
+    g = plan_graph(log_n=11, tokens=64)
+    g.set_shard(8, 1)
+    assert g.shard_info()["ranks_per_group"] == 2
