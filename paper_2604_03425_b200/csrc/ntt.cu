@@ -516,6 +516,11 @@ __device__ __forceinline__ void load_w_blob(double (&w)[15], const double* sp) {
 #ifndef AEGIS_BLOB_R1
 #define AEGIS_BLOB_R1 0
 #endif
+// fwd_b_fin: L2 prefetch of the finish operands at tile start (-0.4..0.6 % per
+// key switch; the same idea as an L1 prefetch of fwd_b_km's key words cost 5 %)
+#ifndef AEGIS_FIN_PREFETCH
+#define AEGIS_FIN_PREFETCH 1
+#endif
 struct WArr {
   const double* w;
   __device__ __forceinline__ double2 operator()(int sg, int q, double pinv) const {
@@ -736,6 +741,16 @@ __device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin&
   const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
   u64* blk = rr.ptr + (size_t)(chunk * 16 + hi) * 256;
+#if AEGIS_FIN_PREFETCH
+  {  // the finish operands (one 128-byte line per thread each) start moving to
+     // L2 now, while the NTT pass runs
+    const u32 lane = lane_v / F.comps, comp = lane_v - lane * F.comps;
+    const size_t s0 = (size_t)chunk * 4096 + (hi << 8) + 16 * lo;
+    prefetch_l2(F.x + (long long)lane * F.x_lane + (long long)comp * F.x_comp + (size_t)slot * L.n + s0);
+    if (F.add && comp < F.add_comps)
+      prefetch_l2(F.add + (long long)lane * F.add_lane + (long long)comp * F.add_comp + (size_t)slot * L.n + s0);
+  }
+#endif
   double x[16], w[15];
 #pragma unroll
   for (int v = 0; v < 16; ++v) x[v] = dbits(blk[lo + 16 * v]);
