@@ -165,6 +165,13 @@ __device__ __forceinline__ void st256g(u64* p, u64 a, u64 b, u64 c, u64 d) {
   asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
 
+// read-only, no L1 allocation (data shared across CTAs through L2 only)
+__device__ __forceinline__ void ld256na(const u64* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
+}
+
 // cache prefetches (no registers, no completion tracking)
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }

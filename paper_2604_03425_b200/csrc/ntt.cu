@@ -521,6 +521,19 @@ __device__ __forceinline__ void load_w_blob(double (&w)[15], const double* sp) {
 #ifndef AEGIS_FIN_PREFETCH
 #define AEGIS_FIN_PREFETCH 1
 #endif
+#ifndef AEGIS_KM_EXT_CS
+#define AEGIS_KM_EXT_CS 0
+#endif
+// fwd_b_fin finish operands: read once, no L1 allocation (-0.6..1.2 %)
+#ifndef AEGIS_FIN_NA
+#define AEGIS_FIN_NA 1
+#endif
+// fwd_b_km key words: read-only, shared across lanes through L2, no L1
+// allocation (L1 is what the 2 x 102 KB SMEM leaves; the allocating loads
+// thrashed it: -7 % Relin, -8 % non-hoisted Rot)
+#ifndef AEGIS_KM_KEY_NA
+#define AEGIS_KM_KEY_NA 1
+#endif
 struct WArr {
   const double* w;
   __device__ __forceinline__ double2 operator()(int sg, int q, double pinv) const {
@@ -788,12 +801,20 @@ __device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin&
 #pragma unroll
   for (int k = 0; k < 4; ++k) {  // 4 positions at a time keeps the live state small
     u64 xv[4];
+#if AEGIS_FIN_NA
+    ld256na(xr + 4 * k, xv[0], xv[1], xv[2], xv[3]);
+#else
     ld256(xr + 4 * k, xv[0], xv[1], xv[2], xv[3]);
+#endif
     double z[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) z[i] = mm(u2d(xv[i]) - x[4 * k + i], f, fp, p);
     if (has_add) {
+#if AEGIS_FIN_NA
+      ld256na(ar + 4 * k, xv[0], xv[1], xv[2], xv[3]);
+#else
       ld256(ar + 4 * k, xv[0], xv[1], xv[2], xv[3]);
+#endif
 #pragma unroll
       for (int i = 0; i < 4; ++i) z[i] += u2d(xv[i]);
     }
@@ -935,7 +956,11 @@ __global__ void __launch_bounds__(256, 2) fwd_b_km(const KmB K) {
       const u32 idx = j * K.nslots - lo_j + (t < lo_j ? t : t - (hi_j - lo_j));
       const u64* blk = K.ext + (size_t)lane * K.ext_ls + (size_t)idx * K.n + (size_t)(chunk * 16 + hi) * 256;
 #pragma unroll
+#if AEGIS_KM_EXT_CS
+      for (int v = 0; v < 16; ++v) y[v] = dbits(__ldcs(blk + lo + 16 * v));
+#else
       for (int v = 0; v < 16; ++v) y[v] = dbits(blk[lo + 16 * v]);
+#endif
       double w[15];
 #if AEGIS_BLOB_R1
       if (!blob_ready) {
@@ -964,7 +989,11 @@ __global__ void __launch_bounds__(256, 2) fwd_b_km(const KmB K) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       u64 a, b, c, dd;
+#if AEGIS_KM_KEY_NA
+      ld256na(k0 + 4 * k, a, b, c, dd);
+#else
       ld256(k0 + 4 * k, a, b, c, dd);
+#endif
       const double w0 = u2d(a), w1 = u2d(b), w2 = u2d(c), w3 = u2d(dd);
       acc0[4 * k] += mm(y[4 * k], w0, w0 * pinv, p);
       acc0[4 * k + 1] += mm(y[4 * k + 1], w1, w1 * pinv, p);
@@ -974,7 +1003,11 @@ __global__ void __launch_bounds__(256, 2) fwd_b_km(const KmB K) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       u64 a, b, c, dd;
+#if AEGIS_KM_KEY_NA
+      ld256na(k0 + kcomp + 4 * k, a, b, c, dd);
+#else
       ld256(k0 + kcomp + 4 * k, a, b, c, dd);
+#endif
       const u64 kk[4] = {a, b, c, dd};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
