@@ -754,6 +754,9 @@ __device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin&
   const double p = sc->pd, pinv = sc->pinv;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
   u64* blk = rr.ptr + (size_t)(chunk * 16 + hi) * 256;
+  // the finish factor is a dynamically indexed kernel parameter (an LDC that
+  // stalled the epilogue): fetch it now, its latency hides under the NTT
+  const u64 f_bits = F.f[slot];
 #if AEGIS_FIN_PREFETCH
   {  // the finish operands (one 128-byte line per thread each) start moving to
      // L2 now, while the NTT pass runs
@@ -789,7 +792,7 @@ __device__ __forceinline__ void tile_fwd_b_fin(const NttLaunch& L, const NttFin&
   const u32 lane = lane_v / F.comps, comp = lane_v - lane * F.comps;
   const u32 sl = (hi << 8) + 16 * lo;                   // this thread's first position inside the tile
   const size_t s0 = (size_t)chunk * 4096 + sl;          // ... inside the limb
-  const double f = u2d(F.f[slot]), fp = f * pinv;
+  const double f = u2d(f_bits), fp = f * pinv;
   const bool has_add = F.add && comp < F.add_comps;
   const u64* xr = F.x + (long long)lane * F.x_lane + (long long)comp * F.x_comp + (size_t)slot * L.n + s0;
   const u64* ar = has_add ? F.add + (long long)lane * F.add_lane + (long long)comp * F.add_comp + (size_t)slot * L.n + s0
