@@ -245,20 +245,15 @@ __global__ void __launch_bounds__(256) basis_convert_kernel(const ConvPlanDev* _
 // sources are replaced in place by xt_i = x_i (B/b_i)^{-1} mod b_i and the
 // overflow count v = round(sum xt_i / b_i) is written to vbuf.  The fused
 // conversion + NTT pass (ntt.cu cfwd_a) then needs only k+1 MACs per target.
+// one source coefficient x of `lane`: x~_i in place (split form) and v
 template <int K>
-__global__ void __launch_bounds__(256) conv_prep_kernel(const ConvPlanDev* __restrict__ pl,
-                                                        const u64* __restrict__ hat_tab, ConvIO io, u64* vbuf,
-                                                        size_t v_ls, u32 lanes, u32 n, u32 m) {
-  const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= lanes * n) return;
-  const u32 lane = gid / n, x = gid - lane * n;
-  u64* src = const_cast<u64*>(io.src) + (size_t)lane * io.src_lane_stride + x;
-  u64 xt[K];
+__device__ __forceinline__ void conv_prep_one(const ConvPlanDev* __restrict__ pl, const u64* __restrict__ hat_tab,
+                                              u32 m, const u64 (&raw)[K], u64 (&xt)[K], u64& v) {
   u64 F_lo = 0, F_hi = 0;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const u64 b = pl->src_p[i];
-    const u64 t = shoup(src[(size_t)io.src_off[i] * n], pl->hat_inv[i], pl->hat_inv_p[i], b);
+    const u64 t = shoup(raw[i], pl->hat_inv[i], pl->hat_inv_p[i], b);
     xt[i] = t;
     const u64 f = t * pl->w_hi[i] + __umul64hi(t, pl->w_lo[i]);
     F_lo += f;
@@ -266,11 +261,37 @@ __global__ void __launch_bounds__(256) conv_prep_kernel(const ConvPlanDev* __res
   }
   const u64 half = 1ull << 63;
   u64 low = F_lo + half;
-  u64 v = F_hi + (low < half);
+  v = F_hi + (low < half);
   if (low >= (u64)0 - 2ull * K) v = tie_resolve(pl, hat_tab + (size_t)2 * K * m, xt, K, v);
+}
+
+// two consecutive coefficients per thread (128-bit loads / stores: twice the
+// bytes in flight of the one-coefficient form, which was latency-bound)
+template <int K>
+__global__ void __launch_bounds__(256) conv_prep_kernel(const ConvPlanDev* __restrict__ pl,
+                                                        const u64* __restrict__ hat_tab, ConvIO io, u64* vbuf,
+                                                        size_t v_ls, u32 lanes, u32 n, u32 m) {
+  const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 half_n = n / 2;
+  if (gid >= lanes * half_n) return;
+  const u32 lane = gid / half_n, x = (gid - lane * half_n) * 2;
+  u64* src = const_cast<u64*>(io.src) + (size_t)lane * io.src_lane_stride + x;
+  u64 ra[K], rb[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) src[(size_t)io.src_off[i] * n] = (xt[i] & 0xFFFFFFull) | ((xt[i] >> 24) << 32);
-  vbuf[(size_t)lane * v_ls + x] = v;  // v <= k < 2^24: already in split form
+  for (int i = 0; i < K; ++i) {
+    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(src + (size_t)io.src_off[i] * n);
+    ra[i] = w.x;
+    rb[i] = w.y;
+  }
+  u64 xa[K], xb[K], va, vb;
+  conv_prep_one<K>(pl, hat_tab, m, ra, xa, va);
+  conv_prep_one<K>(pl, hat_tab, m, rb, xb, vb);
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    *reinterpret_cast<ulonglong2*>(src + (size_t)io.src_off[i] * n) =
+        make_ulonglong2((xa[i] & 0xFFFFFFull) | ((xa[i] >> 24) << 32), (xb[i] & 0xFFFFFFull) | ((xb[i] >> 24) << 32));
+  // v <= k < 2^24: already in split form
+  *reinterpret_cast<ulonglong2*>(vbuf + (size_t)lane * v_ls + x) = make_ulonglong2(va, vb);
 }
 
 // ---------------------------------------------------------------------------
@@ -628,7 +649,7 @@ cudaError_t launch_basis_convert(const ConvPlanDev* plan, const u64* hat_tables,
 
 cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, const ConvIO& io, u64* vbuf,
                              size_t v_ls, u32 lanes, u32 n, u32 k, u32 m, cudaStream_t st) {
-  const size_t total = (size_t)lanes * n;
+  const size_t total = (size_t)lanes * (n / 2);
   if (!total) return cudaSuccess;
   const unsigned grid = (unsigned)((total + 255) / 256);
   switch (k) {
