@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/aegis_params.h"
@@ -172,6 +173,10 @@ __device__ __forceinline__ void ld256na(const u64* p, u64& a, u64& b, u64& c, u6
                : "l"(p));
 }
 
+// programmatic dependent launch: block until the preceding grid in the stream
+// has completed and its writes are visible (a no-op for ordinary launches)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // cache prefetches (no registers, no completion tracking)
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
@@ -203,6 +208,26 @@ __device__ __forceinline__ u64 f64_canon(double x, double p, double pinv) {
   r = r < 0.0 ? r + p : r;
   r = r >= p ? r - p : r;
   return (u64)__double_as_longlong(r + kF64Two52) & 0xFFFFFFFFFFFFFULL;
+}
+
+extern int g_pdl;  // programmatic dependent launch of the key-switch kernels (AEGIS_PDL)
+
+// launch with the programmatic-stream-serialization attribute: the grid may be
+// scheduled while its predecessor drains; the kernel must pdl_wait() before it
+// touches any data an earlier kernel produces or consumes
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 #endif  // __CUDACC__

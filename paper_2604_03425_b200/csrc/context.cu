@@ -101,6 +101,7 @@ Context::Context(const aegis_params& prm, int dev) {
   if (const char* impl = std::getenv("AEGIS_NTT_IMPL")) g_ntt_impl = std::string(impl) == "int" ? kNttInt : kNttF64;
   if (const char* v2 = std::getenv("AEGIS_NTT_V2")) g_ntt_v2 = std::string(v2) != "0";
   if (const char* cf = std::getenv("AEGIS_CONV_FUSED")) g_conv_fused = std::string(cf) != "0";
+  if (const char* pd = std::getenv("AEGIS_PDL")) g_pdl = std::string(pd) != "0";
   if (const char* kf = std::getenv("AEGIS_KM_F64")) g_km_f64 = std::string(kf) != "0";
   if (const char* wsv = std::getenv("AEGIS_WS_SCALE")) ws_scale = std::max(0.001, std::atof(wsv));
   if (const char* ks = std::getenv("AEGIS_KM_SPLIT")) g_km_split = std::string(ks) != "0";

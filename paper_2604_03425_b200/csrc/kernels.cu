@@ -271,6 +271,7 @@ template <int K>
 __global__ void __launch_bounds__(256) conv_prep_kernel(const ConvPlanDev* __restrict__ pl,
                                                         const u64* __restrict__ hat_tab, ConvIO io, u64* vbuf,
                                                         size_t v_ls, u32 lanes, u32 n, u32 m) {
+  pdl_wait();
   const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
   const u32 half_n = n / 2;
   if (gid >= lanes * half_n) return;
@@ -339,6 +340,7 @@ __global__ void keymul_kernel(const KeyMulIO io, u32 lanes, u32 n, const PrimeCo
 template <int DN>
 __global__ void __launch_bounds__(256) keymul_dn2_kernel(const KeyMulIO io, u32 lanes, u32 n,
                                                          const PrimeConst* __restrict__ pc) {
+  pdl_wait();
   const u32 chunks = n / 512;
   const u32 lane = blockIdx.x % lanes, rest = blockIdx.x / lanes;
   const u32 chunk = rest % chunks, slot = rest / chunks;
@@ -653,10 +655,10 @@ cudaError_t launch_conv_prep(const ConvPlanDev* plan, const u64* hat_tables, con
   if (!total) return cudaSuccess;
   const unsigned grid = (unsigned)((total + 255) / 256);
   switch (k) {
-    case 1: conv_prep_kernel<1><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
-    case 2: conv_prep_kernel<2><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
-    case 3: conv_prep_kernel<3><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
-    case 4: conv_prep_kernel<4><<<grid, 256, 0, st>>>(plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 1: launch_pdl(conv_prep_kernel<1>, dim3(grid), dim3(256), 0, st, plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 2: launch_pdl(conv_prep_kernel<2>, dim3(grid), dim3(256), 0, st, plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 3: launch_pdl(conv_prep_kernel<3>, dim3(grid), dim3(256), 0, st, plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
+    case 4: launch_pdl(conv_prep_kernel<4>, dim3(grid), dim3(256), 0, st, plan, hat_tables, io, vbuf, v_ls, lanes, n, m); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -666,15 +668,15 @@ cudaError_t launch_keymul(const KeyMulIO& io, u32 lanes, u32 n, const PrimeConst
   if (g_km_f64 && n >= 512 && io.dnum >= 1 && io.dnum <= 9) {
     const size_t g = (size_t)lanes * io.nslots * (n / 512);
     switch (io.dnum) {
-      case 1: keymul_dn2_kernel<1><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 2: keymul_dn2_kernel<2><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 3: keymul_dn2_kernel<3><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 4: keymul_dn2_kernel<4><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 5: keymul_dn2_kernel<5><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 6: keymul_dn2_kernel<6><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 7: keymul_dn2_kernel<7><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      case 8: keymul_dn2_kernel<8><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
-      default: keymul_dn2_kernel<9><<<(unsigned)g, 256, 0, st>>>(io, lanes, n, pc); break;
+      case 1: launch_pdl(keymul_dn2_kernel<1>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 2: launch_pdl(keymul_dn2_kernel<2>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 3: launch_pdl(keymul_dn2_kernel<3>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 4: launch_pdl(keymul_dn2_kernel<4>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 5: launch_pdl(keymul_dn2_kernel<5>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 6: launch_pdl(keymul_dn2_kernel<6>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 7: launch_pdl(keymul_dn2_kernel<7>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      case 8: launch_pdl(keymul_dn2_kernel<8>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
+      default: launch_pdl(keymul_dn2_kernel<9>, dim3((unsigned)g), dim3(256), 0, st, io, lanes, n, pc); break;
     }
     return cudaGetLastError();
   }

@@ -40,6 +40,7 @@ namespace aegis {
 int g_ntt_impl = kNttF64;
 int g_ntt_v2 = 1;
 int g_conv_fused = 1;
+int g_pdl = 1;
 int g_km_split = 1;
 
 namespace {
@@ -927,6 +928,7 @@ __global__ void __launch_bounds__(256, 2) fwd_b_km(const KmB K) {
   blob_init(&mbar);
   __syncthreads();
   blob_issue(&mbar, stw, K.tw[e].fb + (size_t)chunk * kNttBlobTile);
+  pdl_wait();
   bool blob_ready = false;
   const u32 lo = threadIdx.x & 15, hi = threadIdx.x >> 4;
   const size_t s0 = (size_t)(chunk * 16 + hi) * 256 + 16 * lo;
@@ -1044,6 +1046,7 @@ template <int KB = 8>
 __global__ void __launch_bounds__(256, 3) fwd_a(const NttLaunch L) {
   __shared__ double sm[16 * kStride];
   u32 slot;
+  pdl_wait();
   tile_fwd_a<KB>(L, slot_major(L, blockIdx.x >> (KB - 4), slot), blockIdx.x & ((1u << (KB - 4)) - 1), sm);
 }
 __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
@@ -1055,6 +1058,7 @@ __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
   blob_init(&mbar);
   __syncthreads();
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].fb + (size_t)chunk * kNttBlobTile);
+  pdl_wait();  // the twiddle blob is a constant table: its copy overlaps the predecessor's tail
   tile_fwd_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
 __global__ void __launch_bounds__(256, 2) fwd_b_fin(const NttLaunch L, const NttFin F) {
@@ -1065,6 +1069,7 @@ __global__ void __launch_bounds__(256, 2) fwd_b_fin(const NttLaunch L, const Ntt
   blob_init(&mbar);
   __syncthreads();
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[L.prime[slot]].fb + (size_t)chunk * kNttBlobTile);
+  pdl_wait();
   tile_fwd_b_fin(L, F, lane_v, slot, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
 __global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
@@ -1080,12 +1085,14 @@ __global__ void __launch_bounds__(256, 3) inv_b(const NttLaunch L) {
   blob_init(&mbar);
   __syncthreads();
   blob_issue(&mbar, dyn + 16 * kStride, L.tw[rr.prime].ib + (size_t)chunk * kNttBlobTile);
+  pdl_wait();
   tile_inv_b(L, rr, src, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
 template <int KB = 8>
 __global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
   __shared__ double sm[16 * kStride];
   u32 slot;
+  pdl_wait();
   tile_inv_a<KB>(L, slot_major(L, blockIdx.x >> (KB - 4), slot), blockIdx.x & ((1u << (KB - 4)) - 1), sm);
 }
 
@@ -1094,6 +1101,7 @@ __global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
 template <int K, int T>
 __global__ void __launch_bounds__(256, 3) cfwd_a(const NttLaunch L, const NttConvIn C) {
   extern __shared__ double dyn[];  // exchange rows + (T-1) x 4096 parked targets
+  pdl_wait();
   const u32 groups = (L.nslots + T - 1) / T;
   const u32 grp = blockIdx.x % groups, rest = blockIdx.x / groups;
   const u32 slot0 = grp * T, nt = L.nslots - slot0 < (u32)T ? L.nslots - slot0 : (u32)T;
@@ -1121,11 +1129,11 @@ cudaError_t run(const NttLaunch& L, bool inverse, cudaStream_t st) {
   const u32 rows = L.nlanes * L.nslots;
   const dim3 grid(rows * 16), block(256);
   if (!inverse) {
-    fwd_a<8><<<grid, block, 0, st>>>(L);
-    fwd_b<<<grid, block, kSmemB, st>>>(L);
+    launch_pdl(fwd_a<8>, grid, block, 0, st, L);
+    launch_pdl(fwd_b, grid, block, kSmemB, st, L);
   } else {
-    inv_b<<<grid, block, kSmemB, st>>>(L);
-    inv_a<8><<<grid, block, 0, st>>>(L);
+    launch_pdl(inv_b, grid, block, kSmemB, st, L);
+    launch_pdl(inv_a<8>, grid, block, 0, st, L);
   }
   return cudaGetLastError();
 }
@@ -1260,7 +1268,7 @@ cudaError_t run17(const NttLaunch& L, bool inverse, cudaStream_t st) {
 
 cudaError_t run_km(const KmB& K, cudaStream_t st) {
   init_attrs();
-  fwd_b_km<<<K.nlanes * 16 * K.nslots, 256, kSmemKm, st>>>(K);
+  launch_pdl(fwd_b_km, dim3(K.nlanes * 16 * K.nslots), dim3(256), kSmemKm, st, K);
   return cudaGetLastError();
 }
 
@@ -1271,23 +1279,23 @@ cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, 
   const size_t smem = (size_t)(16 * kStride) * sizeof(double) + (size_t)(T - 1) * 4096 * sizeof(u64);
   const dim3 cgrid(L.nlanes * 16 * ((L.nslots + T - 1) / T));
   switch (C.k) {
-    case 1: cfwd_a<1, T><<<cgrid, block, smem, st>>>(L, C); break;
-    case 2: cfwd_a<2, T><<<cgrid, block, smem, st>>>(L, C); break;
-    case 3: cfwd_a<3, T><<<cgrid, block, smem, st>>>(L, C); break;
-    case 4: cfwd_a<4, T><<<cgrid, block, smem, st>>>(L, C); break;
+    case 1: launch_pdl(cfwd_a<1, T>, cgrid, block, smem, st, L, C); break;
+    case 2: launch_pdl(cfwd_a<2, T>, cgrid, block, smem, st, L, C); break;
+    case 3: launch_pdl(cfwd_a<3, T>, cgrid, block, smem, st, L, C); break;
+    case 4: launch_pdl(cfwd_a<4, T>, cgrid, block, smem, st, L, C); break;
     default: return cudaErrorInvalidValue;
   }
   if (pass_a_only) return cudaGetLastError();
-  if (fin) fwd_b_fin<<<grid, block, kSmemB, st>>>(L, *fin);
-  else fwd_b<<<grid, block, kSmemB, st>>>(L);
+  if (fin) launch_pdl(fwd_b_fin, grid, block, kSmemB, st, L, *fin);
+  else launch_pdl(fwd_b, grid, block, kSmemB, st, L);
   return cudaGetLastError();
 }
 
 cudaError_t run_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) {
   init_attrs();
   const dim3 grid(L.nlanes * L.nslots * 16), block(256);
-  fwd_a<8><<<grid, block, 0, st>>>(L);
-  fwd_b_fin<<<grid, block, kSmemB, st>>>(L, fin);
+  launch_pdl(fwd_a<8>, grid, block, 0, st, L);
+  launch_pdl(fwd_b_fin, grid, block, kSmemB, st, L, fin);
   return cudaGetLastError();
 }
 
