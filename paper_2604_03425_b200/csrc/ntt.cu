@@ -436,11 +436,16 @@ __device__ __forceinline__ double mm(double y, double w, double wp, double p) {
   return fma(-q, p, h) + l;
 }
 __device__ __forceinline__ double red(double x, double p, double pinv) { return fma(-rnd(x * pinv), p, x); }
+// canonical residue: one FP64 reduction, then the two range corrections on
+// the idle integer pipe (r + 1.5 * 2^52 carries the integer r, |r| < 2^51, in
+// its low mantissa bits; the compare/select form cost 4 more FP64-pipe ops)
 __device__ __forceinline__ u64 canon(double x, double p, double pinv) {
-  double r = red(x, p, pinv);
-  r = r < 0.0 ? r + p : r;
-  r = r >= p ? r - p : r;
-  return (u64)__double_as_longlong(r + kTwo52) & 0xFFFFFFFFFFFFFULL;
+  const double r = red(x, p, pinv);  // integer-valued, in (-p, p)
+  const long long pi = __double_as_longlong(p + kTwo52) & 0xFFFFFFFFFFFFFLL;
+  long long y = __double_as_longlong(r + kMagic) - 0x4338000000000000LL;
+  y = y < 0 ? y + pi : y;
+  y = y >= pi ? y - pi : y;
+  return (u64)y;
 }
 
 // Radix-16 rounds.  TW(sg, q) returns the twiddle of stage sg, group q.
