@@ -204,10 +204,13 @@ __device__ __forceinline__ double f64_mulmod(double y, double w, double wp, doub
 }
 // |x| < 2^51 -> canonical residue
 __device__ __forceinline__ u64 f64_canon(double x, double p, double pinv) {
-  double r = fma(-((x * pinv + kF64Magic) - kF64Magic), p, x);
-  r = r < 0.0 ? r + p : r;
-  r = r >= p ? r - p : r;
-  return (u64)__double_as_longlong(r + kF64Two52) & 0xFFFFFFFFFFFFFULL;
+  const double r = fma(-((x * pinv + kF64Magic) - kF64Magic), p, x);  // integer in (-p, p)
+  // range corrections on the integer pipe (r + 1.5 * 2^52 carries r in its mantissa)
+  const long long pi = __double_as_longlong(p + kF64Two52) & 0xFFFFFFFFFFFFFLL;
+  long long y = __double_as_longlong(r + kF64Magic) - 0x4338000000000000LL;
+  y = y < 0 ? y + pi : y;
+  y = y >= pi ? y - pi : y;
+  return (u64)y;
 }
 
 extern int g_pdl;  // programmatic dependent launch of the key-switch kernels (AEGIS_PDL)
