@@ -91,6 +91,35 @@ __global__ void cmult_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b
   }
 }
 
+// 4 contiguous coefficients per thread, 256-bit accesses, streaming stores
+// (the tensor product is HBM-bound: 7 limb streams per limb).  n % 1024 == 0.
+__global__ void __launch_bounds__(256) cmult4_kernel(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb,
+                                                     u32 nlanes, u32 limbs, u32 n, const PrimeConst* __restrict__ pc) {
+  const u32 cpr = n / 1024;
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, l = row / limbs;
+  const PrimeConst P = pc[lb];
+  const u32 la = ma.at(l, nlanes), lbn = mb.at(l, nlanes);
+  const u32 x = (chunk * 256 + threadIdx.x) * 4;
+  u64 a0[4], a1[4], b0[4], b1[4];
+  ld256g(a.limb(la, 0, lb, n) + x, a0[0], a0[1], a0[2], a0[3]);  // operands may be wrapped: keep them cacheable
+  ld256g(a.limb(la, 1, lb, n) + x, a1[0], a1[1], a1[2], a1[3]);
+  ld256g(b.limb(lbn, 0, lb, n) + x, b0[0], b0[1], b0[2], b0[3]);
+  ld256g(b.limb(lbn, 1, lb, n) + x, b1[0], b1[1], b1[2], b1[3]);
+  u64 d0[4], d1[4], d2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d0[i] = mul_mod(a0[i], b0[i], P.p, P.mu104);
+    u128 s = mul_wide(a0[i], b1[i]);
+    mac(s, a1[i], b0[i]);
+    d1[i] = reduce104(s, P.p, P.mu104);
+    d2[i] = mul_mod(a1[i], b1[i], P.p, P.mu104);
+  }
+  st256cs(out.limb(out_lane0 + l, 0, lb, n) + x, d0[0], d0[1], d0[2], d0[3]);
+  st256cs(out.limb(out_lane0 + l, 1, lb, n) + x, d1[0], d1[1], d1[2], d1[3]);
+  st256cs(out.limb(out_lane0 + l, 2, lb, n) + x, d2[0], d2[1], d2[2], d2[3]);
+}
+
 // 8 contiguous coefficients per thread with 256-bit accesses (HBM-bound).
 // The accumulator / first operand streams (evict-first) so a wrapped second
 // operand (e.g. the 48 product lanes added into 1,536 score lanes) stays in L2.
@@ -578,6 +607,12 @@ cudaError_t launch_automorphism(View out, LaneMap om, View in, LaneMap im, u32 n
 
 cudaError_t launch_cmult(View out, u32 out_lane0, View a, LaneMap ma, View b, LaneMap mb, u32 nlanes,
                          u32 limbs, u32 n, const PrimeConst* pc, cudaStream_t st) {
+  if (n % 1024 == 0) {
+    const size_t g = (size_t)nlanes * limbs * (n / 1024);
+    if (!g) return cudaSuccess;
+    cmult4_kernel<<<(unsigned)g, 256, 0, st>>>(out, out_lane0, a, ma, b, mb, nlanes, limbs, n, pc);
+    return cudaGetLastError();
+  }
   const u32 cpr = chunks_of(n);
   const size_t g = (size_t)nlanes * limbs * cpr;
   if (!g) return cudaSuccess;
