@@ -1066,7 +1066,10 @@ __global__ void __launch_bounds__(256, 3) fwd_b(const NttLaunch L) {
   pdl_wait();  // the twiddle blob is a constant table: its copy overlaps the predecessor's tail
   tile_fwd_b(L, rr, chunk, dyn, dyn + 16 * kStride, &mbar, 0);
 }
-__global__ void __launch_bounds__(256, 2) fwd_b_fin(const NttLaunch L, const NttFin F) {
+#ifndef AEGIS_FIN_MINB
+#define AEGIS_FIN_MINB 2
+#endif
+__global__ void __launch_bounds__(256, AEGIS_FIN_MINB) fwd_b_fin(const NttLaunch L, const NttFin F) {
   extern __shared__ double dyn[];
   __shared__ u64 mbar;
   const u32 row = blockIdx.x >> 4, chunk = blockIdx.x & 15;
@@ -1103,8 +1106,11 @@ __global__ void __launch_bounds__(256, 3) inv_a(const NttLaunch L) {
 
 // fused conversion + pass A, one launch per pass: tiles ordered (lane, chunk,
 // slot fastest) so the CTAs converting one lane's column chunk run together
+#ifndef AEGIS_CFWD_MINB
+#define AEGIS_CFWD_MINB 3  // resident CTAs per SM the register cap is sized for
+#endif
 template <int K, int T>
-__global__ void __launch_bounds__(256, 3) cfwd_a(const NttLaunch L, const NttConvIn C) {
+__global__ void __launch_bounds__(256, AEGIS_CFWD_MINB) cfwd_a(const NttLaunch L, const NttConvIn C) {
   extern __shared__ double dyn[];  // exchange rows + (T-1) x 4096 parked targets
   pdl_wait();
   const u32 groups = (L.nslots + T - 1) / T;
