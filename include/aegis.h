@@ -157,6 +157,11 @@ int aegis_graph_info(const aegis_graph* g, uint64_t* ops, uint64_t* bundles);
  * with world = m * groups the m ranks of a group split its positions and each
  * PCMM is reduce-scattered once through the reducer hook.  world <= 1 clears. */
 int aegis_graph_set_shard(aegis_graph* g, uint32_t world, uint32_t rank);
+/* Parity of one token group inside an UNSHARDED run: every lane is still
+ * computed, but bundle hashes (aegis_graph_run) cover only the lanes of token
+ * group `group` (as aegis_graph_set_shard(token groups, group) would own
+ * them).  group < 0 restores whole-bundle hashes. */
+int aegis_graph_set_hash_group(aegis_graph* g, int32_t group);
 /* reduce-scatter hook: sum words_per_rank*m u64 words at device pointer `buf`
  * over the m ranks of token group `group` (NCCL uint64 sum), leaving this
  * rank's share at buf + part*words_per_rank; return 0 on success. */

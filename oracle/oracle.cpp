@@ -30,6 +30,7 @@
 #include <vector>
 
 #include <omp.h>
+#include <sys/mman.h>
 
 #include "../include/aegis_params.h"
 
@@ -762,9 +763,36 @@ struct GOp {
   u32 use_level;
   std::vector<Slice> ins;
 };
+// Zero-initialised bundle storage backed by an anonymous mapping: pages are
+// committed only when written, so a lane-subset run (orc_run_graph_tg) holds
+// just the lanes it computes even though lane addressing stays dense.
+struct LazyBuf {
+  u64* p = nullptr;
+  size_t bytes = 0;
+  LazyBuf() = default;
+  LazyBuf(const LazyBuf&) = delete;
+  LazyBuf& operator=(const LazyBuf&) = delete;
+  LazyBuf(LazyBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  ~LazyBuf() { release(); }
+  void assign(size_t words) {
+    release();
+    if (!words) return;
+    bytes = words * sizeof(u64);
+    void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (m == MAP_FAILED) throw std::runtime_error("oracle: bundle mapping failed");
+    p = (u64*)m;
+  }
+  void release() {
+    if (p) munmap(p, bytes);
+    p = nullptr;
+    bytes = 0;
+  }
+  u64* data() { return p; }
+};
+
 struct GBundle {
   u32 id, lanes, level, comps, chunk = 0;
-  std::vector<u64> data;  // [lane][comps_alloc][level][N]
+  LazyBuf data;  // [lane][comps_alloc][level][N]
   u32 comps_alloc = 0;
   u32 cur_comps = 0;
   bool live = false;
@@ -829,6 +857,74 @@ struct Exec {
   std::vector<int64_t> last_use;
   uint64_t* hashes;
   uint64_t nhashes;
+  // Lane-subset mode (orc_run_graph_tg): compute and hash only the lanes of
+  // token group tg_sel.  Token-coherent placement (placement.hpp:175-182,
+  // PAPER.md:406-421) restated independently of the product: a graph input's
+  // lanes are token-major (lane / (lanes / tg_total)); a PCMM output lane
+  // lane(t, o) belongs to t; every other output lane inherits the group of the
+  // operand lane it reads (emit_per_lane, he_ir.hpp:200-222).
+  u32 tg_total = 1;
+  int tg_sel = -1;
+  std::vector<std::vector<int32_t>> tag;  // [bundle][lane]
+
+  bool owns(u32 b, u32 lane) const { return tg_sel < 0 || tag[b][lane] == tg_sel; }
+  void tag_lanes() {
+    tag.assign(g.b.size(), {});
+    for (auto& b : g.b) tag[b.id].assign(b.lanes, -1);
+    for (u32 id : g.inputs) {
+      const u32 lanes = g.b[id].lanes;
+      if (lanes % tg_total) throw std::logic_error("graph input lanes not a multiple of token groups");
+      for (u32 l = 0; l < lanes; ++l) tag[id][l] = (int32_t)(l / (lanes / tg_total));
+    }
+    auto put = [&](u32 b, u32 lane, int32_t t) {
+      if (tag[b][lane] >= 0 && tag[b][lane] != t) throw std::logic_error("lane written by two token groups");
+      tag[b][lane] = t;
+    };
+    for (const GOp& o : g.ops) {
+      if (o.kind == kEncode) continue;
+      const u32 nl = o.out.count;
+      if (o.kind == kPMult) {
+        const Pcmm s = pcmm(o);
+        for (u32 t = 0; t < s.tg; ++t)
+          for (u32 oo = 0; oo < s.c_out; ++oo) put(o.out.b, o.out.lane + s.lane(t, oo), (int32_t)t);
+        continue;
+      }
+      for (u32 l = 0; l < nl; ++l) {
+        const int32_t t = tag[o.ins[0].b][map_lane(o.ins[0], l, nl)];
+        if (t < 0) throw std::logic_error("op reads an untagged lane");
+        for (size_t k = 1; k < o.ins.size(); ++k)
+          if (tag[o.ins[k].b][map_lane(o.ins[k], l, nl)] != t)
+            throw std::invalid_argument("op " + std::to_string(o.id) + " couples token groups: no lane-subset run");
+        put(o.out.b, o.out.lane + l, t);
+      }
+    }
+  }
+  struct Pcmm {
+    u32 tg, c_in, c_out, S, c_sub, chunk;
+    u32 lane(u32 t, u32 oo) const { return S == 1 ? t * c_out + oo : (oo / c_sub) * chunk + t * c_sub + oo % c_sub; }
+  };
+  Pcmm pcmm(const GOp& o) const {
+    const u64 in_l = o.ins[0].count, out_l = o.out.count, w_l = o.ins[1].count;
+    u64 tg = 1;
+    while (tg * tg * w_l < in_l * out_l) ++tg;
+    if (tg * tg * w_l != in_l * out_l || in_l % tg || out_l % tg)
+      throw std::logic_error("PMult lane shapes inconsistent");
+    Pcmm s;
+    s.tg = (u32)tg;
+    s.c_in = (u32)(in_l / tg);
+    s.c_out = (u32)(out_l / tg);
+    if ((u64)s.c_in * s.c_out != w_l) throw std::logic_error("PMult weight lanes inconsistent");
+    s.chunk = g.b[o.out.b].chunk;
+    s.S = (s.chunk == 0 || s.chunk >= out_l) ? 1 : (u32)(out_l / s.chunk);
+    if (s.c_out % s.S) throw std::logic_error("PMult sub-tensor split inconsistent");
+    s.c_sub = s.c_out / s.S;
+    return s;
+  }
+  // keys are regenerated on demand; keep the cache bounded at production size
+  void trim_keys() {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->key_cache.size() * (size_t)n * 8 > ((size_t)6 << 30)) c->key_cache.clear();
+  }
 
   u64* lane_ptr(GBundle& b, u32 lane, u32 comp = 0) {
     return b.data.data() + ((size_t)lane * b.comps_alloc + comp) * b.level * n;
@@ -836,7 +932,7 @@ struct Exec {
   void ensure(GBundle& b, u32 comps) {
     if (b.live) return;
     b.comps_alloc = std::max(b.comps, comps);
-    b.data.assign((size_t)b.lanes * b.comps_alloc * b.level * n, 0);
+    b.data.assign((size_t)b.lanes * b.comps_alloc * b.level * n);
     b.live = true;
     b.cur_comps = b.comps_alloc;
   }
@@ -845,19 +941,31 @@ struct Exec {
 #pragma omp parallel for collapse(2) num_threads(c->threads)
     for (long ln = 0; ln < (long)b.lanes; ++ln)
       for (long cp = 0; cp < 2; ++cp)
-        for (u32 lb = 0; lb < b.level; ++lb)
+        for (u32 lb = 0; lb < b.level && owns(b.id, (u32)ln); ++lb)
           orc_input_limb(c, b.id, (u32)ln, (u32)cp, lb, lane_ptr(b, (u32)ln, (u32)cp) + (size_t)lb * n);
   }
   void finish(GBundle& b) {
     if (!b.live) return;
-    if (b.id < nhashes)
-      hashes[b.id] = orc_hash_bundle_data(b.data.data(), b.lanes, b.comps_alloc, b.cur_comps, b.level,
-                                          b.level, n);
-    std::vector<u64>().swap(b.data);
+    if (b.id < nhashes) {
+      // DESIGN.md §2.4 over the owned lanes only (all lanes when tg_sel < 0)
+      u64 h = 0;
+      for (u32 ln = 0; ln < b.lanes; ++ln) {
+        if (!owns(b.id, ln)) continue;
+        for (u32 cp = 0; cp < b.cur_comps; ++cp)
+          for (u32 lb = 0; lb < b.level; ++lb) {
+            const u64* src = lane_ptr(b, ln, cp) + (size_t)lb * n;
+            const u64 base = (((u64)ln * b.cur_comps + cp) * b.level + lb) * n;
+            for (u32 x = 0; x < n; ++x) h += mix64(src[x] + (base + x) * kGold);
+          }
+      }
+      hashes[b.id] = h;
+    }
+    b.data.release();
     b.live = false;
   }
 
   void run(int64_t max_ops) {
+    if (tg_sel >= 0) tag_lanes();
     last_use.assign(g.b.size(), -1);
     for (size_t i = 0; i < g.ops.size(); ++i) {
       last_use[g.ops[i].out.b] = (int64_t)i;
@@ -897,12 +1005,14 @@ struct Exec {
     ensure(out, 2);
     const u32 L = o.use_level, nl = o.out.count;
     // pre-generate key limbs (shared by all lanes)
+    trim_keys();
     for (u32 j = 0; j < dnum_of(L); ++j)
       for (u32 cp = 0; cp < 2; ++cp)
         for (u32 e = 0; e < L + AEGIS_SPECIAL_PRIMES; ++e)
           key_limb(c, 1000u + (u64)o.rot, j, cp, e < L ? e : kSpecialBase + (e - L));
 #pragma omp parallel for num_threads(c->threads) schedule(dynamic, 1)
     for (long l = 0; l < (long)nl; ++l) {
+      if (!owns(o.out.b, o.out.lane + (u32)l)) continue;
       const u32 il = map_lane(o.ins[0], (u32)l, nl);
       std::vector<u64> src(2 * (size_t)L * n), dst(2 * (size_t)L * n);
       for (u32 cp = 0; cp < 2; ++cp)
@@ -918,6 +1028,7 @@ struct Exec {
   void relin_op(const GOp& o) {
     GBundle& b = g.b[o.out.b];
     const u32 L = o.use_level, nl = o.out.count;
+    trim_keys();
     for (u32 j = 0; j < dnum_of(L); ++j)
       for (u32 cp = 0; cp < 2; ++cp)
         for (u32 e = 0; e < L + AEGIS_SPECIAL_PRIMES; ++e)
@@ -925,6 +1036,7 @@ struct Exec {
     const size_t cstride = (size_t)b.level * n;
 #pragma omp parallel for num_threads(c->threads) schedule(dynamic, 1)
     for (long l = 0; l < (long)nl; ++l) {
+      if (!owns(o.out.b, o.out.lane + (u32)l)) continue;
       u64* p = lane_ptr(b, o.out.lane + (u32)l);
       std::vector<u64> res(2 * cstride);
       relin(c, p, L, cstride, res.data(), cstride);
@@ -942,6 +1054,7 @@ struct Exec {
 #pragma omp parallel for collapse(2) num_threads(c->threads)
     for (long l = 0; l < (long)nl; ++l)
       for (long i = 0; i < (long)L; ++i) {
+        if (!owns(o.out.b, o.out.lane + (u32)l)) continue;
         const u32 la = map_lane(o.ins[0], (u32)l, nl), lb = map_lane(o.ins[1], (u32)l, nl);
         const u64 q = c->prime[i];
         const u64* a0 = lane_ptr(a, la, 0) + i * n; const u64* a1 = lane_ptr(a, la, 1) + i * n;
@@ -967,6 +1080,7 @@ struct Exec {
 #pragma omp parallel for collapse(2) num_threads(c->threads) schedule(dynamic, 1)
     for (long l = 0; l < (long)nl; ++l)
       for (long cp = 0; cp < 2; ++cp) {
+        if (!owns(o.out.b, o.out.lane + (u32)l)) continue;
         const u32 il = map_lane(o.ins[0], (u32)l, nl);
         rescale_poly(c, lane_ptr(in, il, (u32)cp), L, lane_ptr(out, o.out.lane + (u32)l, (u32)cp));
       }
@@ -981,6 +1095,7 @@ struct Exec {
 #pragma omp parallel for collapse(2) num_threads(c->threads) schedule(dynamic, 1)
     for (long l = 0; l < (long)nl; ++l)
       for (long cp = 0; cp < 2; ++cp) {
+        if (!owns(o.out.b, o.out.lane + (u32)l)) continue;
         const u32 il = map_lane(o.ins[0], (u32)l, nl);
         boot_poly(c, lane_ptr(in, il, (u32)cp), L, out.level, lane_ptr(out, o.out.lane + (u32)l, (u32)cp));
       }
@@ -999,6 +1114,7 @@ struct Exec {
     for (long l = 0; l < (long)nl; ++l)
       for (long cp = 0; cp < 2; ++cp)
         for (long i = 0; i < (long)L; ++i) {
+          if (!owns(o.out.b, o.out.lane + (u32)l)) continue;
           const u64 q = c->prime[i];
           u64* d = lane_ptr(out, o.out.lane + (u32)l, (u32)cp) + i * n;
           GBundle& a = g.b[o.ins[0].b];
@@ -1025,20 +1141,10 @@ struct Exec {
     ensure(acc, 2);
     GBundle& X = g.b[o.ins[0].b];
     const u32 wb = o.ins[1].b;
-    const u64 in_l = o.ins[0].count, out_l = o.out.count, w_l = o.ins[1].count;
-    u64 tg = 1;
-    while (tg * tg * w_l < in_l * out_l) ++tg;
-    if (tg * tg * w_l != in_l * out_l || in_l % tg || out_l % tg)
-      throw std::logic_error("PMult lane shapes inconsistent");
-    const u32 c_in = (u32)(in_l / tg), c_out = (u32)(out_l / tg);
-    if ((u64)c_in * c_out != w_l) throw std::logic_error("PMult weight lanes inconsistent");
+    const Pcmm s = pcmm(o);
+    const u32 c_in = s.c_in, c_out = s.c_out, tg = s.tg;
     const u32 L = o.use_level;
-    const u32 S = (acc.chunk == 0 || acc.chunk >= out_l) ? 1 : (u32)(out_l / acc.chunk);
-    if (c_out % S) throw std::logic_error("PMult sub-tensor split inconsistent");
-    const u32 c_sub = c_out / S;
-    auto acc_lane = [&](u32 t, u32 oo) {
-      return S == 1 ? t * c_out + oo : (oo / c_sub) * acc.chunk + t * c_sub + oo % c_sub;
-    };
+    auto acc_lane = [&](u32 t, u32 oo) { return s.lane(t, oo); };
 #pragma omp parallel for collapse(2) num_threads(c->threads) schedule(dynamic, 1)
     for (long i = 0; i < (long)L; ++i)
       for (long oo = 0; oo < (long)c_out; ++oo) {
@@ -1047,7 +1153,7 @@ struct Exec {
         for (u32 ci = 0; ci < c_in; ++ci)
           orc_weight_limb(c, wb, ci * c_out + (u32)oo, (u32)i, w.data() + (size_t)ci * n);
         for (u32 t = 0; t < tg; ++t)
-          for (u32 cp = 0; cp < 2; ++cp) {
+          for (u32 cp = 0; cp < 2 && (tg_sel < 0 || (int)t == tg_sel); ++cp) {
             u64* d = lane_ptr(acc, o.out.lane + acc_lane(t, (u32)oo), cp) + i * n;
             for (u32 x = 0; x < n; ++x) {
               u128 s = d[x];
@@ -1065,8 +1171,16 @@ struct Exec {
 
 extern "C" int64_t orc_run_graph(orc_ctx* c, const char* path, int64_t max_ops, uint64_t* hashes,
                                  uint64_t nhashes) {
+  return orc_run_graph_tg(c, path, max_ops, hashes, nhashes, 1, -1);
+}
+
+extern "C" int64_t orc_run_graph_tg(orc_ctx* c, const char* path, int64_t max_ops, uint64_t* hashes,
+                                    uint64_t nhashes, uint32_t tg_total, int32_t tg_sel) {
   try {
+    if (tg_total == 0 || tg_sel >= (int32_t)tg_total) throw std::invalid_argument("bad token-group selection");
     Exec ex{c, parse(path), c->n, {}, hashes, nhashes};
+    ex.tg_total = tg_total;
+    ex.tg_sel = tg_sel;
     if (hashes) std::fill(hashes, hashes + nhashes, 0);
     ex.run(max_ops);
     return (int64_t)ex.g.b.size();

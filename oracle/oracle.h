@@ -85,6 +85,11 @@ void orc_input_limb(orc_ctx* c, uint32_t bundle, uint32_t lane, uint32_t comp, u
  * bundles, or < 0 on error (message via orc_last_error). */
 int64_t orc_run_graph(orc_ctx* c, const char* path, int64_t max_ops, uint64_t* hashes,
                       uint64_t nhashes);
+/* Lane-subset form: computes and hashes only the lanes of token group tg_sel
+ * (of tg_total), tagged by the oracle's own restatement of token-coherent
+ * placement (placement.hpp:175-182).  tg_sel < 0 = every lane (orc_run_graph). */
+int64_t orc_run_graph_tg(orc_ctx* c, const char* path, int64_t max_ops, uint64_t* hashes,
+                         uint64_t nhashes, uint32_t tg_total, int32_t tg_sel);
 uint64_t orc_hash_bundle_data(const uint64_t* data, uint32_t lanes, uint32_t comps_stride,
                               uint32_t comps, uint32_t level_stride, uint32_t level, uint32_t n);
 const char* orc_last_error(void);

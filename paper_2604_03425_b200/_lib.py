@@ -71,6 +71,7 @@ SIGNATURES = [
     ("aegis_graph_dump", ctypes.c_int, [vp, ctypes.c_char_p]),
     ("aegis_graph_info", ctypes.c_int, [vp, u64p, u64p]),
     ("aegis_graph_set_shard", ctypes.c_int, [vp, u32, u32]),
+    ("aegis_graph_set_hash_group", ctypes.c_int, [vp, ctypes.c_int32]),
     ("aegis_graph_set_reducer", ctypes.c_int, [vp, vp, vp]),
     ("aegis_graph_owned_lanes", ctypes.c_int, [vp, u32, ctypes.POINTER(ctypes.c_uint8), u32]),
     ("aegis_graph_shard_info", ctypes.c_int, [vp, u32p, u32p, u32p, u32p, u32p]),

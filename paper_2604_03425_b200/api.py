@@ -270,6 +270,12 @@ class Graph:
         if rc:
             _raise(rc, self.lib.aegis_last_error(None).decode())
 
+    def set_hash_group(self, group):
+        """Unsharded run, hashes over the lanes of token group `group` only (-1: all)."""
+        rc = self.lib.aegis_graph_set_hash_group(self.h, group)
+        if rc:
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+
     def shard_info(self):
         v = [ctypes.c_uint32() for _ in range(5)]
         self.lib.aegis_graph_shard_info(self.h, *[ctypes.byref(x) for x in v])

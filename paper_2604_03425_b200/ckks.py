@@ -162,6 +162,8 @@ class Ckks:
         self.ctx.keys_upload(0, self.key(negacyclic_int(self.s, self.s)))
 
     def upload_rotation_key(self, r):
+        if r <= -500:  # key ids >= 500 mark rotation keys (1000 + r, poly_ir.hpp:300-305)
+            raise ValueError("rotation offset must be > -500")
         k = pow(5, r % self.n, 2 * self.n)
         self.ctx.keys_upload(1000 + r, self.key(automorphism_int(self.s, k)))
 

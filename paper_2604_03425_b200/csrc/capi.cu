@@ -85,6 +85,7 @@ struct aegis_graph {
   std::string header;
   uint64_t peak = 0;
   std::unique_ptr<aegis::ShardPlan> shard;
+  std::unique_ptr<aegis::ShardPlan> hash_lanes;  // aegis_graph_set_hash_group
   aegis::ReduceFn reduce = nullptr;
   void* reduce_user = nullptr;
   int hoist = 1;
@@ -111,6 +112,7 @@ uint32_t token_groups(const aegis_graph* g) {
 void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   Context& c = *ctx->c;
   opt.shard = g->shard.get();
+  opt.hash_lanes = g->hash_lanes.get();
   opt.reduce = g->reduce;
   opt.reduce_user = g->reduce_user;
   opt.hoist = g->hoist != 0;
@@ -314,6 +316,7 @@ int aegis_keyswitch(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* in, u
     Bundle& o = need(out);
     const Bundle& i = need(in);
     if (comp >= i.comps || o.comps < 2 || o.lanes != i.lanes) throw Error(AEGIS_EINVAL, "keyswitch: bad shapes");
+    if (&o == &i) throw Error(AEGIS_EINVAL, "keyswitch: out must not alias in (the finish scatters over its input)");
     check_level(i, level, "keyswitch");
     check_level(o, level, "keyswitch");
     const u32 n = ctx->c->n;
@@ -356,6 +359,8 @@ int aegis_rot(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_
     check_lanes(i, in_lane, lanes, "rot");
     check_level(i, level, "rot");
     check_level(o, level, "rot");
+    if (&o == &i && out_lane < in_lane + lanes && in_lane < out_lane + lanes)
+      throw Error(AEGIS_EINVAL, "rot: output lanes overlap the input lanes (the automorphism scatter is not in-place)");
     ctx->c->op_rot(o, out_lane, i, LaneMap{in_lane, lanes}, lanes, level, offset);
   });
 }
@@ -533,6 +538,18 @@ int aegis_graph_set_shard(aegis_graph* g, uint32_t world, uint32_t rank) {
     g->shard.reset(new aegis::ShardPlan(aegis::make_shard_plan(g->g, token_groups(g), world, rank)));
   });
 }
+int aegis_graph_set_hash_group(aegis_graph* g, int32_t group) {
+  if (!g) return AEGIS_EINVAL;
+  return guard(nullptr, [&] {
+    if (group < 0) {
+      g->hash_lanes.reset();
+      return;
+    }
+    const uint32_t tg = token_groups(g);
+    if ((uint32_t)group >= tg) throw Error(AEGIS_EINVAL, "token group out of range");
+    g->hash_lanes.reset(new aegis::ShardPlan(aegis::make_shard_plan(g->g, tg, tg, (uint32_t)group)));
+  });
+}
 int aegis_graph_set_reducer(aegis_graph* g, aegis_reduce_fn fn, void* user) {
   if (!g) return AEGIS_EINVAL;
   g->reduce = reinterpret_cast<aegis::ReduceFn>(fn);  // uint64_t* and u64* are the same 64-bit words
@@ -597,7 +614,10 @@ int aegis_graph_key_ids(const aegis_graph* g, uint64_t* ids, uint32_t cap, uint3
   if (!g || !n) return AEGIS_EINVAL;
   std::set<uint64_t> s;
   for (const hp::HeOp& op : g->g.ops) {
-    if (op.kind == hp::HeOpKind::kRot) s.insert(1000u + (uint64_t)(int64_t)op.rot_offset);
+    if (op.kind == hp::HeOpKind::kRot) {
+      if (op.rot_offset <= -500) return AEGIS_EINVAL;  // validate_heops rejects these at load
+      s.insert(1000u + (uint64_t)(int64_t)op.rot_offset);
+    }
     if (op.kind == hp::HeOpKind::kRelin) s.insert(0);
   }
   uint32_t k = 0;

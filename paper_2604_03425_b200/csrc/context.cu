@@ -758,7 +758,7 @@ void Context::op_rot_cached(Bundle& out, u32 out_lane, const Bundle& in, LaneMap
                             int offset, const u64* ext) {
   if (level > in.level || level > out.level) throw Error(AEGIS_EINVAL, "rotation level exceeds operand level");
   const u64 gk = galois_of(offset);
-  const u64 key_id = 1000u + (u64)(long long)offset;
+  const u64 key_id = rotation_key_id(offset);
   const size_t in_ls = (size_t)in.comps * in.level * n;
   KsOut o;
   o.out_lane[0] = o.out_lane[1] = (size_t)out.comps * out.level * n;

@@ -130,6 +130,12 @@ class Context {
   void ks_core(const u64* ext, const u64* d, size_t d_ls, u32 lanes, u32 level, const u64* key, u64 galois,
                const KsOut& o, bool ext_pass_a = false);
   u64 galois_of(int offset) const;
+  // key id of rotation r (poly_ir.hpp:300-305: 1000 + r).  Ids >= 500 mark
+  // rotation keys (stored pre-permuted), so offsets <= -500 are rejected.
+  static u64 rotation_key_id(int offset) {
+    if (offset <= -500) throw Error(AEGIS_EINVAL, "rotation offset must be > -500 (key id 1000 + r)");
+    return 1000u + (u64)(long long)offset;
+  }
 
   // ---- HE operators --------------------------------------------------------
   void op_rot(Bundle& out, u32 out_lane, const Bundle& in, LaneMap im, u32 lanes, u32 level, int offset);

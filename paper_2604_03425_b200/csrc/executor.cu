@@ -44,6 +44,7 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
     }
   }
   if (o.shard && !o.shard->active()) o.shard = nullptr;
+  if (o.hash_lanes && o.shard) throw Error(AEGIS_EINVAL, "hash lane selection applies to unsharded runs only");
   find_hoist_groups();
   if (o.dce) find_live_lanes();
 }
@@ -134,14 +135,23 @@ void Executor::retire(u32 id) {
       d2h_bytes += (size_t)(e - s) * lane_words * 8;
     }
   }
-  if (o.d_hash) {
-    for (auto [s, e] : runs) {
-      AEGIS_CHECK_CUDA(launch_hash(b.view(), s, e - s, cur_comps[id], cb.level, c.n, o.d_hash + id, c.stream));
-      c.count();
-    }
-  }
+  if (o.d_hash) hash_bundle(id, b);
   c.free_bundle(buf[id]);
   buf[id] = nullptr;
+}
+
+// DESIGN.md §2.4 content hash of the lanes this rank owns (or, with
+// hash_lanes, of that plan's lanes only) into o.d_hash[id]
+void Executor::hash_bundle(u32 id, const Bundle& b) {
+  const u32 lanes = g.bundles[id].lanes;
+  const ShardPlan* hp_ = o.hash_lanes ? o.hash_lanes : o.shard;
+  std::vector<std::pair<u32, u32>> runs =
+      hp_ ? hp_->runs(id, 0, lanes) : std::vector<std::pair<u32, u32>>{{0, lanes}};
+  for (auto [a, e] : runs) {
+    AEGIS_CHECK_CUDA(launch_hash(b.view(), a, e - a, cur_comps[id], g.bundles[id].level, c.n, o.d_hash + id,
+                                 c.stream));
+    c.count();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -376,15 +386,7 @@ void Executor::donate(const hp::HeOp& op, int64_t i) {
   for (size_t k = 1; k < op.ins.size(); ++k)  // a second operand must not alias differently
     if (op.ins[k].bundle == s.bundle && (op.ins[k].lane != 0 || op.ins[k].lane_count != ob.lanes)) return;
   if (partial[s.bundle]) reduce_partial(s.bundle);
-  if (o.d_hash) {  // the operand dies now: hash it before it is overwritten
-    std::vector<std::pair<u32, u32>> runs =
-        o.shard ? o.shard->runs(s.bundle, 0, in.lanes) : std::vector<std::pair<u32, u32>>{{0, in.lanes}};
-    for (auto [a, e] : runs) {
-      AEGIS_CHECK_CUDA(launch_hash(in.view(), a, e - a, cur_comps[s.bundle], g.bundles[s.bundle].level, c.n,
-                                   o.d_hash + s.bundle, c.stream));
-      c.count();
-    }
-  }
+  if (o.d_hash) hash_bundle(s.bundle, in);  // the operand dies now: hash it before it is overwritten
   buf[op.out.bundle] = buf[s.bundle];  // same allocation, operand strides
   donated[s.bundle] = 1;               // still readable by this op; never freed or hashed again
   cur_comps[op.out.bundle] = 2;

@@ -23,6 +23,9 @@ struct RunOptions {
   const u64* host_in = nullptr;          // graph inputs from host memory
   u64* host_out = nullptr;               // final bundle to host memory
   const ShardPlan* shard = nullptr;
+  // if set, bundle hashes cover only the lanes this plan owns (execution is
+  // unaffected): the unsharded run reports one token group's lanes
+  const ShardPlan* hash_lanes = nullptr;
   ReduceFn reduce = nullptr;
   void* reduce_user = nullptr;
   bool hoist = true;
@@ -54,6 +57,7 @@ class Executor {
   Bundle& get(u32 id);
   Bundle& input(const heplan::LaneSlice& s);
   void retire(u32 id);
+  void hash_bundle(u32 id, const Bundle& b);
   void find_hoist_groups();
   void find_live_lanes();
   bool live_lane(u32 b, u32 lane) const { return !o.dce || live[b][lane]; }

@@ -482,7 +482,45 @@ HeOpGraph parse_heops(const std::string& text) {
       g.ops.push_back(op);
     }
   }
+  validate_heops(g);
   return g;
+}
+
+// Structural checks of a graph from outside the lowering (a heops file or an
+// in-memory graph handed over the C-ABI): every index the executor and the
+// kernels derive from it must stay inside the bundle table, lane ranges and
+// levels.  Violations are std::invalid_argument (AEGIS_EINVAL).
+void validate_heops(const HeOpGraph& g) {
+  const size_t nb = g.bundles.size();
+  auto bad = [](const std::string& m) { throw std::invalid_argument("heops: " + m); };
+  for (size_t i = 0; i < nb; ++i) {
+    const CtBundle& b = g.bundles[i];
+    if (b.id != i) bad("bundle ids must be dense");
+    if (b.lanes == 0 || b.components == 0 || b.components > 3) bad("bundle " + std::to_string(i) + " has a bad shape");
+    if (b.level == 0 || b.level > 64) bad("bundle " + std::to_string(i) + " level out of range");
+  }
+  for (uint32_t in : g.graph_inputs)
+    if (in >= nb) bad("graph input " + std::to_string(in) + " is not a bundle");
+  auto slice_ok = [&](const LaneSlice& s) {
+    return s.bundle < nb && s.lane_count > 0 && (uint64_t)s.lane + s.lane_count <= g.bundles[s.bundle].lanes;
+  };
+  for (const HeOp& op : g.ops) {
+    const std::string at = "op " + std::to_string(op.id);
+    if ((unsigned)op.kind > (unsigned)HeOpKind::kBoot) bad(at + ": unknown kind");
+    if (!slice_ok(op.out)) bad(at + ": output slice outside its bundle");
+    if (op.ins.size() > 4) bad(at + ": too many operands");
+    if (op.kind != HeOpKind::kEncode && op.use_level == 0) bad(at + ": use_level 0");
+    for (const LaneSlice& s : op.ins) {
+      if (!slice_ok(s)) bad(at + ": operand slice outside its bundle");
+      if (op.use_level > g.bundles[s.bundle].level) bad(at + ": use_level above an operand's level");
+    }
+    const bool shrinks = op.kind == HeOpKind::kRescale || op.kind == HeOpKind::kBoot || op.kind == HeOpKind::kEncode;
+    if (!shrinks && op.use_level > g.bundles[op.out.bundle].level) bad(at + ": use_level above the output's level");
+    if (op.kind == HeOpKind::kRescale && op.use_level < 2) bad(at + ": rescale needs two limbs");
+    if (op.kind == HeOpKind::kRot && op.rot_offset <= -500) bad(at + ": rotation offset must be > -500 (key id 1000 + r)");
+    if (op.kind == HeOpKind::kRescale && g.bundles[op.out.bundle].level + 1 < op.use_level)
+      bad(at + ": rescale output level below use_level - 1");
+  }
 }
 
 }  // namespace aegis::heplan

@@ -97,5 +97,6 @@ HeOpGraph lower_app_to_he(const AppGraph& app, const CkksProfile& p, const Packi
 // text round trip in the tests/golden heops format
 std::string dump_heops(const HeOpGraph& g, const std::string& header);
 HeOpGraph parse_heops(const std::string& text);
+void validate_heops(const HeOpGraph& g);  // throws std::invalid_argument
 
 }  // namespace aegis::heplan

@@ -11,6 +11,8 @@ PcmmShape pcmm_shape(uint32_t in_l, uint32_t out_l, uint32_t w_l, uint32_t chunk
   while (tg * tg * w_l < (uint64_t)in_l * out_l) ++tg;
   if (tg * tg * w_l != (uint64_t)in_l * out_l || in_l % tg || out_l % tg)
     throw std::logic_error("PMult lane shapes inconsistent");
+  if (chunk != 0 && chunk < out_l && out_l % chunk != 0)
+    throw std::invalid_argument("PMult chunk_period must divide the accumulator lanes");
   PcmmShape s;
   s.tg = (uint32_t)tg;
   s.c_in = in_l / s.tg;

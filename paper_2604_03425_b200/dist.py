@@ -77,28 +77,36 @@ class P2pReducer:
         if w is not None and w[1] >= nbytes:
             return w[0]
         lib = self.ctx.lib
-        if w is not None:
+        if w is not None:  # forget the old window before freeing it (no second destroy in close())
+            del self.win[group]
             lib.aegis_p2p_destroy(w[0])
         g = self.groups[group]
+        m = dist.get_world_size(g)
         raw = (ctypes.c_char * 64)()
         h = ctypes.c_void_p()
-        self.ctx._call("aegis_p2p_create", nbytes, ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(h))
-        m = dist.get_world_size(g)
-        handles = [None] * m
-        dist.all_gather_object(handles, bytes(raw), group=g)
-        allh = ctypes.create_string_buffer(b"".join(handles), 64 * m)
         err = ""
         try:
-            self.ctx._call("aegis_p2p_open", h, ctypes.cast(allh, ctypes.c_void_p), m, self.part)
+            self.ctx._call("aegis_p2p_create", nbytes, ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(h))
         except Exception as e:  # noqa: BLE001 -- decided collectively below
             err = repr(e)
-        errs = [None] * m
-        dist.all_gather_object(errs, err, group=g)
-        if any(errs):
+            h = ctypes.c_void_p()
+        handles = [None] * m  # every rank reaches this gather, so a local failure cannot hang the others
+        dist.all_gather_object(handles, (bytes(raw), err), group=g)
+        err = next((e for _, e in handles if e), "")
+        if not err:
+            allh = ctypes.create_string_buffer(b"".join(r for r, _ in handles), 64 * m)
+            try:
+                self.ctx._call("aegis_p2p_open", h, ctypes.cast(allh, ctypes.c_void_p), m, self.part)
+            except Exception as e:  # noqa: BLE001 -- decided collectively below
+                err = repr(e)
+            errs = [None] * m
+            dist.all_gather_object(errs, err, group=g)
+            err = next((e for e in errs if e), "")
+        if err:
             import sys
-            print(f"aegis: peer-memory windows unavailable ({next(e for e in errs if e)}); "
-                  "using the NCCL reduce-scatter", file=sys.stderr)
-            lib.aegis_p2p_destroy(h)
+            print(f"aegis: peer-memory windows unavailable ({err}); using the NCCL reduce-scatter", file=sys.stderr)
+            if h.value:
+                lib.aegis_p2p_destroy(h)
             self.fallback = make_reducer(self.groups, self.part)
             return None
         self.win[group] = (h, nbytes)

@@ -48,6 +48,8 @@ def lib():
             "orc_weight_limb": (None, [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u64p]),
             "orc_input_limb": (None, [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u64p]),
             "orc_run_graph": (ctypes.c_int64, [vp, ctypes.c_char_p, ctypes.c_int64, u64p, ctypes.c_uint64]),
+            "orc_run_graph_tg": (ctypes.c_int64, [vp, ctypes.c_char_p, ctypes.c_int64, u64p, ctypes.c_uint64,
+                                                 ctypes.c_uint32, ctypes.c_int32]),
             "orc_hash_bundle_data": (ctypes.c_uint64, [u64p] + [ctypes.c_uint32] * 6),
             "orc_last_error": (ctypes.c_char_p, []),
         }
@@ -196,6 +198,13 @@ class Oracle:
     def run_graph(self, path, max_ops=-1, nbundles=1 << 16):
         h = np.zeros(nbundles, dtype=np.uint64)
         nb = self._chk(self.L.orc_run_graph(self.h, str(path).encode(), max_ops, P(h), nbundles))
+        return h[:nb]
+
+    def run_graph_tg(self, path, tg_total, tg_sel, max_ops=-1, nbundles=1 << 16):
+        """Lanes of token group tg_sel only (hashes over those lanes)."""
+        h = np.zeros(nbundles, dtype=np.uint64)
+        nb = self._chk(self.L.orc_run_graph_tg(self.h, str(path).encode(), max_ops, P(h), nbundles,
+                                               tg_total, tg_sel))
         return h[:nb]
 
 

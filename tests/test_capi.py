@@ -55,3 +55,39 @@ def test_graph_key_ids_cover_rotations_and_relin():
     ids = set(int(x) for x in g.key_ids())
     assert 0 in ids and all(1000 + r in ids for r in range(1, 64))
     assert len(ids) == 64
+
+
+def _load(path):
+    lib = _lib.load()
+    g = ctypes.c_void_p()
+    rc = lib.aegis_graph_load(None, str(path).encode(), ctypes.byref(g))
+    if rc == 0:
+        lib.aegis_graph_free(g)
+    return rc, lib.aegis_last_error(None)
+
+
+def test_graph_load_validates_every_index(tmp_path, golden_dir):
+    """aegis_graph_load (no device needed) accepts every reference-emitted graph
+    and rejects out-of-range bundle / lane / level / offset fields with
+    AEGIS_EINVAL instead of letting the executor index past its tables."""
+    from conftest import golden_graph
+    for name in ("ffn_n10_t8", "block_n11_t32", "block_n16_t2048"):
+        assert _load(golden_graph(name, golden_dir))[0] == 0, name
+    base = open(golden_graph("ffn_n10_t8", golden_dir)).read().splitlines()
+    first_op = next(i for i, ln in enumerate(base) if ln.startswith("O ") and ln.split()[2] == "5")  # a Rot
+    f = base[first_op].split()
+
+    def mutate(idx, value, what):
+        g = list(f)
+        g[idx] = str(value)
+        p = tmp_path / f"bad_{idx}.heops"
+        p.write_text("\n".join(base[:first_op] + [" ".join(g)] + base[first_op + 1:]) + "\n")
+        rc, msg = _load(p)
+        assert rc == _lib.AEGIS_EINVAL, (what, rc)
+        return msg
+
+    nb = sum(1 for ln in base if ln.startswith("B "))
+    mutate(4, nb + 7, "output bundle out of range")          # O id kind rot out.b ...
+    mutate(6, 1 << 20, "output lane count beyond the bundle")
+    mutate(11, 60, "use_level above the operand level")
+    mutate(3, -700, "rotation offset aliasing the relin key ids")

@@ -413,17 +413,32 @@ def test_sharded_execution_matches(world, dce, tmp_path):
     assert len(bad) == 0, f"{len(bad)} bundles differ, first {bad[:5]}"
 
 
+PROD_FIXTURES = ["prod_ffn_n16_t128", "prod_block_n16_t512", "prod_block_n16_t2048_tg0"]
+
+
 @pytest.mark.slow
-def test_graph_parity_config1_production(golden_dir):
-    """Config 1 (FFN 768->3072->768, T=128, N=2^16, l=17..2): a prefix of the op
-    list (first PCMM diagonals) is checked bundle-by-bundle against the oracle."""
-    path = golden_graph("ffn_n16_t128", golden_dir)
-    c = ctx(16)
-    g = c.load_graph(path)
-    ops = 24  # Rot / Encode / PMult for r = 0..7 of ffn1 at level 17
-    h_gpu = g.run(max_ops=ops, hashes=True)
-    h_cpu = orc(16).run_graph(path, max_ops=ops)
-    assert (h_gpu[: len(h_cpu)] == h_cpu).all()
+@pytest.mark.parametrize("fixture", PROD_FIXTURES)
+def test_graph_parity_production(fixture, golden_dir):
+    """BASELINE configs at production size (N = 2^16, L = 35), whole graph,
+    every bundle hash vs the CPU oracle (fixtures from
+    tests/golden/make_prod_hashes.py): config 1 (FFN, T = 128, 426 ops),
+    config 2 (block, T = 512, 1,511 ops) and the headline T = 2048 layer run
+    UNSHARDED exactly as bench.py runs it, hashed over the lanes of token group
+    0 of 4 (the oracle computes only those lanes)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, fixture + ".json")) as f:
+        rec = json.load(f)
+    want = np.array([int(x, 16) for x in rec["hashes"]], dtype=np.uint64)
+    g = ctx(16).load_graph(golden_graph(rec["graph"], golden_dir))
+    if rec["tg_sel"] >= 0:
+        g.set_hash_group(rec["tg_sel"])
+    got = g.run(hashes=True)
+    assert len(got) == len(want) == rec["bundles"]
+    bad = np.nonzero(got != want)[0]
+    assert len(bad) == 0, f"{len(bad)} of {len(want)} bundles differ, first {bad[:8].tolist()}"
+    assert (want != 0).sum() > len(want) // 2  # the fixture covers real data
 
 
 @pytest.mark.parametrize("logn,tokens", [(11, 64), (11, 32)])

@@ -14,6 +14,7 @@ import os
 import numpy as np
 import pytest
 
+from conftest import golden_graph
 from oracle_py import Oracle
 from tools_params import main_primes, special_primes
 
@@ -336,3 +337,25 @@ def test_prng_rows_distinct_and_in_range():
     assert not (orc.weight_limb(5, 4, 2) == w).all()
     k = orc.key_limb(1005, 1, 0, 61)
     assert (k < np.uint64(prime_of(61))).all()
+
+
+def test_token_group_subset_hashes_add_up(golden_dir):
+    """orc_run_graph_tg (the lane-subset oracle used for the T = 2048 fixture)
+    computes each token group independently: the bundle hash is a sum over
+    positions, so the per-group hashes must add up to the
+    whole-graph hashes bit for bit."""
+    path = golden_graph("ffn_n11_t32", golden_dir)
+    orc = Oracle(11)
+    full = orc.run_graph(path)
+    parts = [orc.run_graph_tg(path, 2, t) for t in range(2)]
+    assert all(len(p) == len(full) for p in parts)
+    assert ((parts[0] + parts[1]) == full).all()
+    assert (parts[0] != full).any() and (parts[0] != 0).any()
+
+
+def test_token_group_subset_refuses_coupled_graph(golden_dir):
+    """At T = 32 / N = 2^11 the score tensor has fewer lanes than the product
+    needs per group, so an op reads lanes of both groups: no subset run."""
+    orc = Oracle(11)
+    with pytest.raises(Exception, match="couples token groups"):
+        orc.run_graph_tg(golden_graph("block_n11_t32", golden_dir), 2, 0)
