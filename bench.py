@@ -11,8 +11,11 @@ groups are sharded across ranks (token-coherent placement) and
 `value` is the max-over-ranks device time of the whole layer.
 
 `--impl reference` times the reference path on the host CPU: the reference has
-no executor, so this is the oracle restatement (oracle/, "port"),
-run on a bounded, measured sample of the same layer and extrapolated.
+no executor, so this is the oracle restatement (oracle/, "port")
+of the reference-emitted op list, every op kind measured at the layer's own
+levels on one lane per host thread and scaled by its lane count (measured
+seconds and the extrapolation factor are reported), next to the reference's
+own NegacyclicNtt (oracle/_ref, unmodified) timed on the same cores.
 """
 import argparse
 import json
@@ -125,14 +128,25 @@ def run_reference(args):
 
 
 def _mini_graph(path, kind, level, lanes, c_in=0, c_out=0):
-    """One bundled HE op in the heops text format (he_ir.hpp field order)."""
+    """One bundled HE op at `level` over `lanes` lanes, in the heops text format
+    (field order of he_ir.hpp's HeOp; the same format the reference lowering
+    is dumped in).  Used only to time the CPU oracle on single ops."""
     L = ["# heops v1 calibration", "inputs 0", f"B 0 {lanes} {level} 2 0 0 0 0 in"]
+    one = f"0 0 {lanes}"
     if kind == "rot":
-        L += [f"B 1 {lanes} {level} 2 2 0 0 0 rot", f"O 0 5 1 1 0 {lanes} 0 0 1 0 {level} 0 0 1 0 0 {lanes}"]
-    elif kind == "relin":  # CMult(x, x) then Relin of the product
+        L += [f"B 1 {lanes} {level} 2 2 0 0 0 rot", f"O 0 5 1 1 0 {lanes} 0 0 1 0 {level} 0 0 1 {one}"]
+    elif kind == "cmult":
+        L += [f"B 1 {lanes} {level} 2 1 0 0 0 sq", f"O 0 4 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 2 {one} {one}"]
+    elif kind == "relin":  # CMult(x, x) then Relin of the product (the CMult is timed apart and subtracted)
         L += [f"B 1 {lanes} {level} 2 1 0 0 0 sq",
-              f"O 0 4 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 2 0 0 {lanes} 0 0 {lanes}",
+              f"O 0 4 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 2 {one} {one}",
               f"O 1 6 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 1 1 0 {lanes}"]
+    elif kind == "rescale":
+        L += [f"B 1 {lanes} {level - 1} 2 1 0 0 0 rs", f"O 0 7 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 1 {one}"]
+    elif kind == "cadd":
+        L += [f"B 1 {lanes} {level} 2 1 0 0 0 sum", f"O 0 2 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 2 {one} {one}"]
+    elif kind == "boot":
+        L += [f"B 1 {lanes} 21 2 1 0 0 0 bt", f"O 0 8 0 1 0 {lanes} 0 0 -1 0 {level} 0 0 1 {one}"]
     elif kind == "pmult":
         w = c_in * c_out
         L[2] = f"B 0 {c_in} {level} 2 0 0 0 0 in"
@@ -144,65 +158,130 @@ def _mini_graph(path, kind, level, lanes, c_in=0, c_out=0):
     open(path, "w").write("\n".join(L) + "\n")
 
 
-def cpu_baseline(args, budget_s=20.0, kind=0):
-    """The CPU arm: the oracle (scalar C++ port of the reference semantics, all
-    host threads) timed on single bundled ops of the layer's dominant kinds, then
-    extrapolated over the layer's op list by per-kind lane x level costs."""
-    from oracle_py import Oracle
-    from paper_2604_03425_b200 import plan_graph
-    threads = os.cpu_count() or 1
-    g = plan_graph(log_n=N_LOG, tokens=args.tokens, layers=1, kind=kind)
-    o = Oracle(N_LOG, threads=threads)
-    meas = {}
-    with tempfile.TemporaryDirectory() as d:
-        path = os.path.join(d, "layer.heops")
-        g.dump(path)
-        ops = [ln.split() for ln in open(path) if ln.startswith("O ")]
+def _layer_ops(tokens):
+    """The layer's op list as the UNMODIFIED reference lowering emitted it
+    (tests/golden/block_n16_t<T>.heops.gz, made by tests/golden/make_golden.py
+    from lower_app_to_he, he_ir.hpp:683) -- no libaegis on the reference arm."""
+    import gzip
+    path = os.path.join(ROOT, "tests", "golden", f"block_n16_t{tokens}.heops.gz")
+    with gzip.open(path, "rt") as f:
+        return [ln.split() for ln in f if ln.startswith("O ")], path
 
-        def timed(kind, level, lanes, **kw):
-            mp = os.path.join(d, f"{kind}.heops")
-            _mini_graph(mp, kind, level, lanes, **kw)
-            _mini_graph(os.path.join(d, "none.heops"), "none", level, max(lanes, kw.get("c_in", 0)))
-            o.run_graph(mp)  # untimed: builds NTT tables and the (cached) key limbs
+
+def _fit(points, degree):
+    """least-squares polynomial through measured (level, seconds-per-lane) points"""
+    xs = np.array([p[0] for p in points], dtype=float)
+    ys = np.array([p[1] for p in points], dtype=float)
+    deg = min(degree, len(xs) - 1)
+    c = np.polyfit(xs, ys, deg)
+    return lambda lv: max(float(np.polyval(c, lv)), 0.0)
+
+
+def reference_ntt(threads, limbs=None):
+    """BASELINE.md path (a): the reference's own NegacyclicNtt (rns_math.hpp:44-123,
+    compiled unmodified into oracle/_ref/libheplan_ref.so) on the host cores:
+    forward NTTs of N = 2^16 limbs over the 35 main primes, one limb per thread."""
+    import ctypes
+    from tools_params import main_primes
+    so = os.path.join(ROOT, "oracle", "_ref", "libheplan_ref.so")
+    if not os.path.exists(so):
+        return {"unavailable": "oracle/_ref/libheplan_ref.so not built"}
+    lib = ctypes.CDLL(so)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    lib.ref_ntt_set_create.restype = ctypes.c_void_p
+    lib.ref_ntt_set_create.argtypes = [ctypes.c_uint32, u64p, ctypes.c_uint32]
+    lib.ref_ntt_set_run.argtypes = [ctypes.c_void_p, u64p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int]
+    lib.ref_ntt_set_destroy.argtypes = [ctypes.c_void_p]
+    n = 1 << N_LOG
+    pr = np.array(main_primes()[:35], dtype=np.uint64)
+    t0 = time.time()
+    h = lib.ref_ntt_set_create(n, pr.ctypes.data_as(u64p), len(pr))
+    t_tables = time.time() - t0
+    limbs = limbs or 2 * threads
+    rng = np.random.default_rng(1)
+    data = np.stack([rng.integers(0, int(pr[i % len(pr)]), n, dtype=np.uint64) for i in range(limbs)])
+    t0 = time.time()
+    lib.ref_ntt_set_run(h, data.ctypes.data_as(u64p), limbs, 0, threads)
+    dt = time.time() - t0
+    lib.ref_ntt_set_destroy(h)
+    return {"kind": "reference", "ns_per_limb": dt / limbs * 1e9, "limbs": limbs, "threads": threads,
+            "measured_s": round(dt, 3), "table_build_s": round(t_tables, 3),
+            "gbs_algorithmic": 2 * 8 * n * limbs / dt / 1e9,
+            "what": "heplan::NegacyclicNtt::forward (rns_math.hpp:68-82), unmodified, N=2^16, 35 primes"}
+
+
+def cpu_baseline(args, budget_s=20.0, kind=0):
+    """The CPU arm.  The reference ships no executor, so the layer
+    is run by the oracle (oracle/, a scalar C++ restatement of the reference's
+    semantics, all host threads) op kind by op kind: every Rot / Relin / CMult /
+    Rescale / CAdd / PMult / Boot op of the reference-emitted op list is costed
+    at its own level from a MEASURED single-op sample at that level (one lane
+    per host thread; lanes are independent, so an op's cost is per-lane cost x
+    its lane count).  Levels not sampled are interpolated by a least-squares
+    fit through the sampled ones (quadratic for key switching, linear for the
+    element-wise kinds).  Reported: the sampled seconds, the extrapolated layer
+    seconds and their ratio, plus the reference's own NTT timed beside it."""
+    from oracle_py import Oracle
+    threads = os.cpu_count() or 1
+    ops, src = _layer_ops(args.tokens)
+    o = Oracle(N_LOG, threads=threads)
+    lanes = threads
+    samples = {}
+    measured = 0.0
+    with tempfile.TemporaryDirectory() as d:
+        def run(kind, level, lanes_, **kw):
+            mp = os.path.join(d, f"{kind}_{level}.heops")
+            _mini_graph(mp, kind, level, lanes_, **kw)
+            base = os.path.join(d, f"none_{level}.heops")
+            _mini_graph(base, "none", level, max(lanes_, kw.get("c_in", 0)))
             t0 = time.time()
-            o.run_graph(os.path.join(d, "none.heops"))
-            t_setup = time.time() - t0
+            o.run_graph(base)  # input materialisation only
+            t_in = time.time() - t0
             t0 = time.time()
             o.run_graph(mp)
-            return max(time.time() - t0 - t_setup, 1e-6)
-        lanes = threads  # one lane per host thread
-        meas["rot35"] = timed("rot", 35, lanes) / lanes        # per lane, all threads busy
-        meas["rot17"] = timed("rot", 17, lanes) / lanes
-        meas["relin17"] = timed("relin", 17, lanes) / lanes   # CMult + Relin per lane
-        meas["pmult17"] = timed("pmult", 17, 1, c_in=12, c_out=threads) / (12 * threads)  # per lane-op
-    n = 1 << N_LOG
+            dt = time.time() - t0
+            return max(dt - t_in, 1e-6), dt + t_in
 
-    def ks(level):  # interpolate per-lane key-switch cost ~ a*l + b*l^2 through the two samples
-        b = (meas["rot35"] / 35 - meas["rot17"] / 17) / (35 - 17)
-        a = meas["rot17"] / 17 - b * 17
-        return max(a * level + b * level * level, 0.0)
-
-    def cost(f):
-        kind, lanes, work, lvl = int(f[2]), int(f[6]), int(f[10]), int(f[11])
-        if kind == 5:
-            return ks(lvl) * lanes
-        if kind == 6:
-            return ks(lvl) * lanes  # Relin: one key switch per lane
-        if kind == 3:
-            return meas["pmult17"] * work * lvl / 17
-        if kind == 4:  # CMult: relin17 minus the key switch
-            return max(meas["relin17"] - ks(17), 0.0) * lanes * lvl / 17
-        if kind == 7:  # Rescale ~ (l-1) NTTs + 1 INTT per comp: ~ 2l/(ks NTT count) of a key switch
-            return ks(lvl) * lanes * 2 * lvl / ((-(-lvl // 4) + 3) * lvl + 12)
-        if kind == 8:  # Boot from level 1: 2 x (1 INTT + 20 NTT)
-            return ks(21) * lanes * 42 / ((6 + 3) * 21 + 12)
-        return 0.0
-    value = sum(cost(f) for f in ops) / 1.0
+        _mini_graph(os.path.join(d, "warm.heops"), "rescale", 35, 1)
+        o.run_graph(os.path.join(d, "warm.heops"))  # NTT tables of the main chain (not timed)
+        plan = [("rot", lv) for lv in (2, 17, 30, 34, 35)] + \
+               [("relin", lv) for lv in (3, 9, 17, 25, 34)] + \
+               [("cmult", lv) for lv in (3, 17, 34)] + [("rescale", lv) for lv in (3, 17, 35)] + \
+               [("cadd", lv) for lv in (17, 34)] + [("boot", 1)] + [("pmult", lv) for lv in (2, 17, 35)]
+        for kind_, lv in plan:
+            if kind_ == "pmult":
+                t, w = run("pmult", lv, 1, c_in=12, c_out=lanes)
+                samples.setdefault("pmult", []).append((lv, t / (12 * lanes)))  # per lane-product
+            else:
+                t, w = run(kind_, lv, lanes)
+                samples.setdefault(kind_, []).append((lv, t / lanes))  # per lane
+            measured += w
+        # relin sample = CMult + Relin: subtract the CMult at the same level
+        cm = _fit(samples["cmult"], 1)
+        samples["relin"] = [(lv, max(t - cm(lv), 1e-9)) for lv, t in samples["relin"]]
+    fits = {"rot": _fit(samples["rot"], 2), "relin": _fit(samples["relin"], 2), "cmult": _fit(samples["cmult"], 1),
+            "rescale": _fit(samples["rescale"], 1), "cadd": _fit(samples["cadd"], 1),
+            "boot": _fit(samples["boot"], 0), "pmult": _fit(samples["pmult"], 1)}
+    exact = {k: dict(v) for k, v in samples.items()}
+    names = {2: "cadd", 3: "pmult", 4: "cmult", 5: "rot", 6: "relin", 7: "rescale", 8: "boot"}
+    value = 0.0
+    for f in ops:
+        k, nl, work, lv = int(f[2]), int(f[6]), int(f[10]), int(f[11])
+        nm = names.get(k)
+        if nm is None:
+            continue
+        per = exact.get(nm, {}).get(lv)
+        per = fits[nm](lv) if per is None else per
+        value += per * (work if nm == "pmult" else nl)
+    ntt = reference_ntt(threads)
     return {"value": value, "unit": "s/layer", "cores": threads, "kind": "port",
-            "sample": (f"oracle (CPU port, {threads} threads, one lane per thread) timed on single bundled ops: "
-                       f"Rot at l=35 ({meas['rot35']:.2f}s/lane) and l=17 ({meas['rot17']:.2f}s/lane), "
-                       f"CMult+Relin at l=17, PMult 12x{threads} at l=17; extrapolated over the "
-                       f"{len(ops)} ops of the T={args.tokens} layer by per-kind lane x level costs")}
+            "measured_s": round(measured, 2), "extrapolation": round(value / max(measured, 1e-9), 1),
+            "sample": (f"oracle (CPU port of the reference semantics, {threads} threads, one lane per thread): "
+                       f"{len(plan)} single HE ops timed at the layer's own levels (Rot l=2/17/30/34/35, Relin "
+                       f"3..34, CMult, Rescale, CAdd, Boot, PMult 12x{lanes}); every op of the reference-emitted "
+                       f"op list ({os.path.basename(src)}, {len(ops)} ops) costed as per-lane time at its level x "
+                       f"its lanes (unsampled levels: least-squares fit)"),
+            "reference_ntt": ntt}
 
 
 # ---------------------------------------------------------------------------

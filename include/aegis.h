@@ -60,6 +60,15 @@ int aegis_sync(aegis_ctx* ctx);
 uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t ext_index); /* <60 main, >=60 special */
 /* count of kernels this context launched (for the bench's gpu_launches claim) */
 uint64_t aegis_launch_count(const aegis_ctx* ctx);
+/* Kernel probe (measurement only; one probe per process): kind 1 = cfwd_a
+ * (exact basis conversion fused with NTT pass A), 2 = fwd_b_fin (NTT pass B
+ * with the ModDown / rescale finish), 3 = fwd_b_km (ModUp pass B fused with
+ * the key inner product), 0 = off.  While on, CUDA events bracket every
+ * launch of that kernel on the compute stream; aegis_probe_read returns the
+ * launch count, the summed device time and the summed algorithmic bytes
+ * (inputs read once, outputs written once). */
+int aegis_probe_start(aegis_ctx* ctx, int kind);
+int aegis_probe_read(aegis_ctx* ctx, uint64_t* launches, double* ms, double* alg_bytes);
 /* NTT butterfly arithmetic: 0 = 64-bit integer Shoup, 1 = exact FP64 (default;
  * N = 2^16 uses the direct-access v2 passes), 2 = FP64 through the generic
  * passes.  impl < 0 only queries.  Returns the active implementation. */

@@ -42,6 +42,8 @@ SIGNATURES = [
     ("aegis_sync", ctypes.c_int, [vp]),
     ("aegis_prime", u64, [vp, u32]),
     ("aegis_launch_count", u64, [vp]),
+    ("aegis_probe_start", ctypes.c_int, [vp, ctypes.c_int]),
+    ("aegis_probe_read", ctypes.c_int, [vp, u64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     ("aegis_ntt_impl", ctypes.c_int, [ctypes.c_int]),
     ("aegis_bundle_alloc", ctypes.c_int, [vp, u32, u32, u32, ctypes.POINTER(vp)]),
     ("aegis_bundle_free", ctypes.c_int, [vp, vp]),

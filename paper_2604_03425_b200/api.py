@@ -138,6 +138,18 @@ class Context:
     def launch_count(self):
         return self.lib.aegis_launch_count(self.h)
 
+    PROBE = {"cfwd_a": 1, "fwd_b_fin": 2, "fwd_b_km": 3}
+
+    def probe_start(self, kernel):
+        """Bracket every launch of `kernel` (cfwd_a | fwd_b_fin | fwd_b_km | None) with CUDA events."""
+        self._call("aegis_probe_start", self.PROBE[kernel] if kernel else 0)
+
+    def probe_read(self):
+        """-> (launches, device ms summed over them, algorithmic bytes summed over them)"""
+        n, ms, b = ctypes.c_uint64(), ctypes.c_double(), ctypes.c_double()
+        self._call("aegis_probe_read", ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b))
+        return n.value, ms.value, b.value
+
     # -- bundles / keys --
     def bundle(self, lanes, comps, level):
         h = ctypes.c_void_p()

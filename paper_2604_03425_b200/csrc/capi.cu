@@ -160,6 +160,34 @@ int aegis_sync(aegis_ctx* ctx) {
 }
 uint64_t aegis_prime(const aegis_ctx* ctx, uint32_t e) { return e < aegis::kNumExt ? ctx->c->prime(e) : 0; }
 uint64_t aegis_launch_count(const aegis_ctx* ctx) { return ctx ? ctx->c->launches : 0; }
+
+namespace {
+aegis::KernelProbe g_probe_state;
+}
+int aegis_probe_start(aegis_ctx* ctx, int kind) {
+  return guard(ctx, [&] {
+    if (kind < 0 || kind > aegis::kProbeFwdBKm) throw Error(AEGIS_EINVAL, "unknown probe kind");
+    AEGIS_CHECK_CUDA(cudaStreamSynchronize(ctx->c->stream));
+    for (cudaEvent_t e : g_probe_state.ev) cudaEventDestroy(e);
+    g_probe_state = aegis::KernelProbe{};
+    g_probe_state.kind = kind;
+    aegis::g_probe = kind ? &g_probe_state : nullptr;
+  });
+}
+int aegis_probe_read(aegis_ctx* ctx, uint64_t* launches, double* ms, double* alg_bytes) {
+  return guard(ctx, [&] {
+    AEGIS_CHECK_CUDA(cudaStreamSynchronize(ctx->c->stream));
+    double t = 0;
+    for (size_t i = 0; i + 1 < g_probe_state.ev.size(); i += 2) {
+      float x = 0;
+      AEGIS_CHECK_CUDA(cudaEventElapsedTime(&x, g_probe_state.ev[i], g_probe_state.ev[i + 1]));
+      t += x;
+    }
+    if (launches) *launches = g_probe_state.launches;
+    if (ms) *ms = t;
+    if (alg_bytes) *alg_bytes = g_probe_state.alg_bytes;
+  });
+}
 int aegis_ntt_impl(int impl) {
   if (impl == aegis::kNttInt || impl == aegis::kNttF64) {
     aegis::g_ntt_impl = impl;

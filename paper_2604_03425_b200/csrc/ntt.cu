@@ -1277,9 +1277,28 @@ cudaError_t run17(const NttLaunch& L, bool inverse, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// kernel probe brackets (see KernelProbe)
+inline void probe_mark(int kind, cudaStream_t st) {
+  if (!g_probe || g_probe->kind != kind) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  g_probe->ev.push_back(e);
+}
+inline void probe_done(int kind, cudaStream_t st, double bytes) {
+  if (!g_probe || g_probe->kind != kind) return;
+  probe_mark(kind, st);
+  g_probe->alg_bytes += bytes;
+  ++g_probe->launches;
+}
+
 cudaError_t run_km(const KmB& K, cudaStream_t st) {
   init_attrs();
+  probe_mark(kProbeFwdBKm, st);
   launch_pdl(fwd_b_km, dim3(K.nlanes * 16 * K.nslots), dim3(256), kSmemKm, st, K);
+  // per (lane, slot): dnum digit limbs in, 2 accumulators out; the keys once per launch
+  probe_done(kProbeFwdBKm, st,
+             8.0 * K.n * ((double)K.nlanes * K.nslots * (K.dnum + 2) + 2.0 * K.dnum * K.nslots));
   return cudaGetLastError();
 }
 
@@ -1289,6 +1308,7 @@ cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, 
   constexpr int T = kConvTargets;
   const size_t smem = (size_t)(16 * kStride) * sizeof(double) + (size_t)(T - 1) * 4096 * sizeof(u64);
   const dim3 cgrid(L.nlanes * 16 * ((L.nslots + T - 1) / T));
+  probe_mark(kProbeCfwdA, st);
   switch (C.k) {
     case 1: launch_pdl(cfwd_a<1, T>, cgrid, block, smem, st, L, C); break;
     case 2: launch_pdl(cfwd_a<2, T>, cgrid, block, smem, st, L, C); break;
@@ -1296,9 +1316,18 @@ cudaError_t run_conv(const NttLaunch& L, const NttConvIn& C, const NttFin* fin, 
     case 4: launch_pdl(cfwd_a<4, T>, cgrid, block, smem, st, L, C); break;
     default: return cudaErrorInvalidValue;
   }
+  // k prepared source limbs + the overflow-count row read once per lane, every target limb written once
+  probe_done(kProbeCfwdA, st, 8.0 * L.n * (double)L.nlanes * (L.nslots + C.k + 1));
   if (pass_a_only) return cudaGetLastError();
-  if (fin) launch_pdl(fwd_b_fin, grid, block, kSmemB, st, L, *fin);
-  else launch_pdl(fwd_b, grid, block, kSmemB, st, L);
+  if (fin) {
+    probe_mark(kProbeFwdBFin, st);
+    launch_pdl(fwd_b_fin, grid, block, kSmemB, st, L, *fin);
+    // per (virtual lane, slot): pass-A intermediate + x (+ add) in, out written
+    const double adds = fin->add ? (double)L.nlanes * std::min(fin->add_comps, fin->comps) / fin->comps : 0.0;
+    probe_done(kProbeFwdBFin, st, 8.0 * L.n * (double)L.nslots * (3.0 * L.nlanes + adds));
+  } else {
+    launch_pdl(fwd_b, grid, block, kSmemB, st, L);
+  }
   return cudaGetLastError();
 }
 
@@ -1306,7 +1335,10 @@ cudaError_t run_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) {
   init_attrs();
   const dim3 grid(L.nlanes * L.nslots * 16), block(256);
   launch_pdl(fwd_a<8>, grid, block, 0, st, L);
+  probe_mark(kProbeFwdBFin, st);
   launch_pdl(fwd_b_fin, grid, block, kSmemB, st, L, fin);
+  const double adds = fin.add ? (double)L.nlanes * std::min(fin.add_comps, fin.comps) / fin.comps : 0.0;
+  probe_done(kProbeFwdBFin, st, 8.0 * L.n * (double)L.nslots * (3.0 * L.nlanes + adds));
   return cudaGetLastError();
 }
 
@@ -1356,6 +1388,8 @@ cudaError_t ntt_fwd_fin(const NttLaunch& L, const NttFin& fin, cudaStream_t st) 
   if (L.nlanes * L.nslots == 0) return cudaSuccess;
   return v2::run_fin(L, fin, st);
 }
+
+KernelProbe* g_probe = nullptr;
 
 bool ntt_v2_active(int log_n) { return log_n == 16 && g_ntt_impl == kNttF64 && g_ntt_v2; }
 

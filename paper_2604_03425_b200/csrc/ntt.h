@@ -1,5 +1,7 @@
 // ntt.h -- launch descriptor for the batched NTT (see ntt.cu).
 #pragma once
+
+#include <vector>
 #include "common.cuh"
 
 namespace aegis {
@@ -115,5 +117,18 @@ cudaError_t ntt_fwd_b_keymul(const KmB& k, cudaStream_t st);
 bool ntt_v2_active(int log_n);
 
 cudaError_t ntt_run(const NttLaunch& L, int log_n, bool inverse, cudaStream_t st);
+
+// Kernel probe (measurement only: bench.py's roofline of the step's top
+// kernels).  While g_probe is set, CUDA events bracket every launch of the
+// probed kernel class on its stream and its algorithmic bytes (DESIGN.md §3:
+// each input read once, each output written once) are summed.
+enum ProbeKind { kProbeOff = 0, kProbeCfwdA = 1, kProbeFwdBFin = 2, kProbeFwdBKm = 3 };
+struct KernelProbe {
+  int kind = kProbeOff;
+  std::vector<cudaEvent_t> ev;  // begin/end pairs
+  double alg_bytes = 0;
+  uint64_t launches = 0;
+};
+extern KernelProbe* g_probe;
 
 }  // namespace aegis
