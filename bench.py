@@ -314,6 +314,9 @@ def run_aegis(args):
         g.run()
     barrier()
     l0 = c.launch_count()
+    # the step's dominant kernel (cfwd_a) is timed live inside the
+    # timed region: CUDA events bracket each of its launches on the library stream
+    c.probe_start(TOP_KERNEL)
     with Clocks(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
@@ -322,6 +325,8 @@ def run_aegis(args):
         e1.record(st)
         e1.synchronize()
     barrier()
+    probe = c.probe_read()
+    c.probe_start(None)
     launches = (c.launch_count() - l0) // max(1, args.steps)
     peak_bytes = int(g.peak_bytes())
     ms = e0.elapsed_time(e1) / args.steps
@@ -370,8 +375,9 @@ def run_aegis(args):
         others = {name: time_config(c, st, kind, tokens)
                   for name, kind, tokens in (("config1_ffn_T128", 1, 128), ("config2_layer_T512", 0, 512))}
 
-    # ---- roofline of the dominant kernel (batched NTT), timed on the library stream ----
-    roof = ntt_roofline(c, st)
+    # ---- roofline of the step's dominant kernel (timed live in the step) + the NTT metric ----
+    roof = step_roofline(probe, ms, args.steps, g)
+    roof["ntt"] = ntt_roofline(c, st)
     out = None
     if rank == 0:
         cpu = cpu_baseline(args, budget_s=args.cpu_budget) if (ws == 1 and not args.no_cpu) else None
@@ -439,6 +445,46 @@ def end_to_end(c, g, args, st, barrier):
     return e0.elapsed_time(e1) / steps, h2d, d2h
 
 
+TOP_KERNEL = "cfwd_a"
+
+
+def step_roofline(probe, ms, steps, g):
+    """roofline of the step's top kernel from the live probe: algorithmic bytes
+    (DESIGN.md §3 per-launch model: k prepared source limbs + the overflow row
+    read once per lane, every target limb written once) / its summed device
+    time, against the measured HBM copy bandwidth; `traffic` and the pipe
+    utilisations come from one ncu --set full capture of the same kernel
+    (profiles/r02_cfwd_a_full.json).  `layer` = SURVEY §8(d) algorithmic bytes
+    of the whole replayed op list / step time."""
+    from paper_2604_03425_b200.costs import graph_bytes
+    pk = peaks()
+    n, pms, pbytes = probe
+    out = {"kernel": "cfwd_a<k,2> (exact basis conversion fused with NTT pass A; ModUp / ModDown / rescale "
+                     "targets, DESIGN.md §3.3)", "bound": "hbm", "unit": "GB/s",
+           "peak": pk.get("hbm_gbs"), "peak_source": "measured" if not pk.get("_fallback") else "fallback"}
+    if n and pms > 0:
+        ach = pbytes / (pms / 1e3) / 1e9
+        out.update({"achieved": ach, "frac": ach / pk.get("hbm_gbs"), "launches_per_step": n / max(1, steps),
+                    "avg_launch_us": pms * 1e3 / n, "alg_bytes_per_launch": pbytes / n,
+                    "share_of_step": pms / (ms * max(1, steps))})
+    else:
+        out.update({"achieved": None, "frac": None})
+    out["traffic"] = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r02_cfwd_a_full.json")))
+        out["traffic"] = prof["dram_bytes_per_launch"]
+        out["ncu"] = {k: prof[k] for k in prof if k != "dram_bytes_per_launch"}
+    except Exception:
+        pass
+    _, _, ops, _ = g.export()
+    total, _ = graph_bytes(ops, 1 << N_LOG)
+    ach = total / (ms / 1e3) / 1e9
+    out["layer"] = {"alg_bytes": total, "achieved": ach, "frac": ach / pk.get("hbm_gbs"),
+                    "model": "SURVEY §8(d) per-op bytes summed over the replayed op list "
+                             "(paper_2604_03425_b200/costs.py)"}
+    return out
+
+
 def ntt_roofline(c, st):
     """Forward NTT of 48 lanes x 17 limbs (the FFN1 rotation source shape) --
     the kernel class that dominates the layer's key switching."""
@@ -458,6 +504,10 @@ def ntt_roofline(c, st):
     t = e0.elapsed_time(e1) / reps / 1e3
     limbs = 48 * 17
     alg = 2 * 8 * (1 << N_LOG) * limbs
+    try:
+        fp64_peak = json.load(open(os.path.join(ROOT, "profiles", "r02_pipe_peaks.json")))["dfma_tfma_s"]
+    except Exception:
+        fp64_peak = 148 * 64 * 1.965e9 / 1e12
     achieved = alg / t / 1e9
     b.free()
     traffic = None
@@ -474,8 +524,9 @@ def ntt_roofline(c, st):
             # 8 DFMA-pipe instructions per butterfly, 16 x 32768 butterflies per limb, plus the
             # u64<->f64 conversions (~7 per coefficient); peak = 148 SMs x 64 lanes x max SM clock
             "fp64_pipe": {"achieved_tops": limbs * (16 * 32768 * 8 + 7 * 65536) / t / 1e12,
-                          "peak_tops": 148 * 64 * 1.965e9 / 1e12,
-                          "frac": limbs * (16 * 32768 * 8 + 7 * 65536) / t / (148 * 64 * 1.965e9)}}
+                          "peak_tops": fp64_peak,
+                          "peak_source": "measured DFMA rate (tools/probe/imad_peak.cu, profiles/r02_pipe_peaks.json)",
+                          "frac": limbs * (16 * 32768 * 8 + 7 * 65536) / t / (fp64_peak * 1e12)}}
 
 
 def main():

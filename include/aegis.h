@@ -123,12 +123,65 @@ int aegis_basis_convert(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* i
 int aegis_keyswitch(aegis_ctx* ctx, aegis_bundle* out, const aegis_bundle* in, uint32_t comp,
                     uint32_t level, uint64_t key_id);
 
+/* kLimbMulAdd with its LimbOpcode payload (poly_ir.hpp:49-58), as
+ * HeLowering::pointwise emits it per limb (poly_ir.hpp:192-213), on the
+ * FragSpan out = lanes [out_lane, out_lane + lanes) x limbs [prime_lo,
+ * prime_hi] of `out`; operand lanes follow emit_per_lane (a_count / b_count
+ * lanes starting at a_lane / b_lane).  Plaintext operands are 1-component
+ * bundles: they feed component 0 of Add/Sub and scale every component of
+ * Mul/MulAcc; two ciphertexts Mul into the 3-component tensor ("component
+ * product", poly_ir.hpp:53).  kGenerate fills `out` with the seeded fragment
+ * of bundle id `param` (the executor's kEncode weights); a and b are unused.
+ * kKeyMul is not a standalone instruction here: it runs inside
+ * aegis_keyswitch (the IR's KeyMul has no digit split) and returns EINVAL.
+ * `out` may be `a` only with identical lanes (a_lane == out_lane, a_count ==
+ * lanes); results are canonical residues. */
+#define AEGIS_LIMB_ADD 1      /* out = a + b   */
+#define AEGIS_LIMB_SUB 2      /* out = a - b   */
+#define AEGIS_LIMB_MUL 3      /* out = a * b   */
+#define AEGIS_LIMB_MULACC 4   /* out += a * b  */
+#define AEGIS_LIMB_ADDACC 5   /* out += a      */
+#define AEGIS_LIMB_KEYMUL 6   /* out = a * key(param): inside aegis_keyswitch only */
+#define AEGIS_LIMB_GENERATE 7 /* out = PRNG fragment of bundle `param` */
+int aegis_limb_op(aegis_ctx* ctx, int opcode, aegis_bundle* out, uint32_t out_lane, uint32_t lanes,
+                  const aegis_bundle* a, uint32_t a_lane, uint32_t a_count, const aegis_bundle* b,
+                  uint32_t b_lane, uint32_t b_count, uint32_t prime_lo, uint32_t prime_hi, uint64_t param);
+/* kLimbDrop (poly_ir.hpp:341-354): level -> level - 1.  mode = PolyMode:
+ * 0 (kNone) keeps limbs [0, level - 1) (exact truncation, graph.hpp:106-107);
+ * 3 (kRescaleTail) divides by the dropped prime q_{level-1} and rounds
+ * (= aegis_rescale).  Other modes are EINVAL. */
+#define AEGIS_MODE_NONE 0
+#define AEGIS_MODE_KEY_SWITCH 1
+#define AEGIS_MODE_BOOT_RESET 2
+#define AEGIS_MODE_RESCALE_TAIL 3
+int aegis_limb_drop(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
+                    uint32_t in_lane, uint32_t lanes, uint32_t level, int mode);
+
 /* ---- HE operators (HeOpKind, he_ir.hpp:21-31), one call per bundled HeOp --
  * Operand lanes follow emit_per_lane (he_ir.hpp:200-222): output lane l reads
  * operand lane  lane0 + (count == lanes ? l : l % count).                  */
 int aegis_rot(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
               uint32_t in_lane, uint32_t lanes, uint32_t level, int offset);
+/* Several rotations of the same source lanes (the rotation ladder of
+ * lower_matmul / lower_attention_*, he_ir.hpp:224-241, 328-373): ModUp of the
+ * source is computed once and shared by every offset (hoisting); rotation k
+ * writes lanes [out_lanes[k], out_lanes[k] + lanes) of outs[k].  Bit-identical
+ * to n_offsets separate aegis_rot calls. */
+int aegis_rot_hoisted(aegis_ctx* ctx, aegis_bundle* const* outs, const uint32_t* out_lanes, const int* offsets,
+                      uint32_t n_offsets, const aegis_bundle* in, uint32_t in_lane, uint32_t lanes,
+                      uint32_t level);
 int aegis_relin(aegis_ctx* ctx, aegis_bundle* b, uint32_t lane, uint32_t lanes, uint32_t level);
+/* kPAdd (he_ir.hpp:23): out[l] = ct[..] + pt[..] (pt: 1-component bundle, added to component 0) */
+int aegis_padd(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, uint32_t lanes, const aegis_bundle* ct,
+               uint32_t ct_lane, uint32_t ct_count, const aegis_bundle* pt, uint32_t pt_lane, uint32_t pt_count,
+               uint32_t level);
+/* kEncode (he_ir.hpp:243-252, lowered to kGenerate poly_ir.hpp:310-321): lanes
+ * [lane, lane + lanes) of the plaintext bundle pt (1 component) receive the
+ * weights of bundle id `weight_bundle_id` -- the same words the PMult kernel
+ * generates in-kernel, so a stored-plaintext PCMM reads what the fused one
+ * computes. */
+int aegis_encode(aegis_ctx* ctx, aegis_bundle* pt, uint32_t lane, uint32_t lanes, uint32_t level,
+                 uint32_t weight_bundle_id);
 int aegis_rescale(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
                   uint32_t in_lane, uint32_t lanes, uint32_t level);
 int aegis_boot(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in,
@@ -160,6 +213,45 @@ int aegis_graph_build_params(const aegis_params* params, const aegis_model* mode
 int aegis_graph_load(aegis_ctx* ctx, const char* path, aegis_graph** out); /* heops text */
 int aegis_graph_dump(const aegis_graph* g, const char* path);
 int aegis_graph_info(const aegis_graph* g, uint64_t* ops, uint64_t* bundles);
+/* In-memory HeOpGraph ingest (he_ir.hpp:57-120) -- no text round trip.  The
+ * descriptors mirror CtBundle / LaneSlice / HeOp field for field (enum values
+ * as in he_ir.hpp: HeOpKind, BundleClass, AggregationAxis); bundle ids are the
+ * array indices, op ids the op positions.  `meta` carries the CkksProfile /
+ * layout / model the graph was lowered for (token groups, ring degree).  The
+ * graph is validated (bundle ids, lane ranges, levels) before it is accepted:
+ * EINVAL with the first offending op otherwise.  heplan_compat.hpp builds
+ * these arrays from a heplan::HeOpGraph. */
+typedef struct aegis_graph_meta {
+  uint32_t log_n, chain_length, bootstrap_level, slots_per_token;
+  uint32_t model_dim, head_dim, ffn_dim, layers, kind;
+  uint64_t tokens;
+} aegis_graph_meta;
+typedef struct aegis_bundle_desc {
+  uint32_t lanes, level, components, cls, aggregation, app_node, chunk_period, replicate_hint;
+  const char* tag; /* may be NULL; copied */
+} aegis_bundle_desc;
+typedef struct aegis_slice {
+  uint32_t bundle, lane, lane_count;
+} aegis_slice;
+#define AEGIS_MAX_OP_INPUTS 4
+typedef struct aegis_op_desc {
+  uint32_t kind, accumulate, aligned, aggregation;
+  int32_t rot_offset, phase;
+  aegis_slice out;
+  uint32_t in_count;
+  aegis_slice ins[AEGIS_MAX_OP_INPUTS];
+  uint64_t work;
+  uint32_t use_level, app_node;
+} aegis_op_desc;
+int aegis_graph_from_ops(const aegis_graph_meta* meta, const aegis_bundle_desc* bundles, uint32_t n_bundles,
+                         const aegis_op_desc* ops, uint64_t n_ops, const uint32_t* inputs, uint32_t n_inputs,
+                         aegis_graph** out);
+/* the reverse: copy a graph's bundles / ops / inputs out (caps in elements,
+ * NULL arrays are skipped; *n_inputs receives the input count; tag pointers
+ * stay valid while the graph lives) */
+int aegis_graph_export(const aegis_graph* g, aegis_bundle_desc* bundles, uint32_t bundle_cap, aegis_op_desc* ops,
+                       uint64_t op_cap, uint32_t* inputs, uint32_t input_cap, uint32_t* n_inputs,
+                       aegis_graph_meta* meta);
 /* Multi-GPU token-coherent placement (placement.hpp:175-182):
  * this context executes only the lanes rank `rank` of `world` owns.  With
  * world <= token groups each rank owns whole token groups (no collective);

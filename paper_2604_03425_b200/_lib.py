@@ -32,6 +32,35 @@ class AegisModel(ctypes.Structure):
                 ("head_dim", u32), ("slots_per_token", u32), ("tokens", u64)]
 
 
+class AegisGraphMeta(ctypes.Structure):
+    _fields_ = [("log_n", u32), ("chain_length", u32), ("bootstrap_level", u32), ("slots_per_token", u32),
+                ("model_dim", u32), ("head_dim", u32), ("ffn_dim", u32), ("layers", u32), ("kind", u32),
+                ("tokens", u64)]
+
+
+class AegisBundleDesc(ctypes.Structure):
+    _fields_ = [("lanes", u32), ("level", u32), ("components", u32), ("cls", u32), ("aggregation", u32),
+                ("app_node", u32), ("chunk_period", u32), ("replicate_hint", u32), ("tag", ctypes.c_char_p)]
+
+
+class AegisSlice(ctypes.Structure):
+    _fields_ = [("bundle", u32), ("lane", u32), ("lane_count", u32)]
+
+
+MAX_OP_INPUTS = 4
+
+
+class AegisOpDesc(ctypes.Structure):
+    _fields_ = [("kind", u32), ("accumulate", u32), ("aligned", u32), ("aggregation", u32),
+                ("rot_offset", ctypes.c_int32), ("phase", ctypes.c_int32), ("out", AegisSlice),
+                ("in_count", u32), ("ins", AegisSlice * MAX_OP_INPUTS), ("work", u64), ("use_level", u32),
+                ("app_node", u32)]
+
+
+# LimbOpcode (poly_ir.hpp:49-58) and PolyMode (:60-65) values of the C-ABI
+LIMB_ADD, LIMB_SUB, LIMB_MUL, LIMB_MULACC, LIMB_ADDACC, LIMB_KEYMUL, LIMB_GENERATE = range(1, 8)
+MODE_NONE, MODE_KEY_SWITCH, MODE_BOOT_RESET, MODE_RESCALE_TAIL = range(4)
+
 # (name, restype, argtypes) for every function declared in include/aegis.h
 SIGNATURES = [
     ("aegis_ctx_create", ctypes.c_int, [ctypes.POINTER(AegisParams), ctypes.c_int, ctypes.POINTER(vp)]),
@@ -60,7 +89,13 @@ SIGNATURES = [
     ("aegis_basis_convert", ctypes.c_int, [vp, vp, vp, u32p, u32p, u32, u32p, u32p, u32]),
     ("aegis_keyswitch", ctypes.c_int, [vp, vp, vp, u32, u32, u64]),
     ("aegis_rot", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32, ctypes.c_int]),
+    ("aegis_limb_op", ctypes.c_int, [vp, ctypes.c_int, vp, u32, u32, vp, u32, u32, vp, u32, u32, u32, u32, u64]),
+    ("aegis_limb_drop", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32, ctypes.c_int]),
+    ("aegis_rot_hoisted", ctypes.c_int, [vp, ctypes.POINTER(vp), u32p, ctypes.POINTER(ctypes.c_int), u32, vp, u32,
+                                         u32, u32]),
     ("aegis_relin", ctypes.c_int, [vp, vp, u32, u32, u32]),
+    ("aegis_padd", ctypes.c_int, [vp, vp, u32, u32, vp, u32, u32, vp, u32, u32, u32]),
+    ("aegis_encode", ctypes.c_int, [vp, vp, u32, u32, u32, u32]),
     ("aegis_rescale", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32]),
     ("aegis_boot", ctypes.c_int, [vp, vp, u32, vp, u32, u32, u32, u32]),
     ("aegis_cmult", ctypes.c_int, [vp, vp, u32, u32, vp, u32, u32, vp, u32, u32, u32]),
@@ -72,6 +107,12 @@ SIGNATURES = [
     ("aegis_graph_load", ctypes.c_int, [vp, ctypes.c_char_p, ctypes.POINTER(vp)]),
     ("aegis_graph_dump", ctypes.c_int, [vp, ctypes.c_char_p]),
     ("aegis_graph_info", ctypes.c_int, [vp, u64p, u64p]),
+    ("aegis_graph_from_ops", ctypes.c_int,
+     [ctypes.POINTER(AegisGraphMeta), ctypes.POINTER(AegisBundleDesc), u32, ctypes.POINTER(AegisOpDesc), u64, u32p,
+      u32, ctypes.POINTER(vp)]),
+    ("aegis_graph_export", ctypes.c_int,
+     [vp, ctypes.POINTER(AegisBundleDesc), u32, ctypes.POINTER(AegisOpDesc), u64, u32p, u32, u32p,
+      ctypes.POINTER(AegisGraphMeta)]),
     ("aegis_graph_set_shard", ctypes.c_int, [vp, u32, u32]),
     ("aegis_graph_set_hash_group", ctypes.c_int, [vp, ctypes.c_int32]),
     ("aegis_graph_set_reducer", ctypes.c_int, [vp, vp, vp]),

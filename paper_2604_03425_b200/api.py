@@ -195,6 +195,38 @@ class Context:
         self._call("aegis_rot", out.h, out_lane, inp.h, in_lane,
                    inp.lanes if lanes is None else lanes, level, offset)
 
+    def rot_hoisted(self, outs, inp, offsets, level, out_lanes=None, in_lane=0, lanes=None):
+        """Rotations of one source by several offsets, ModUp shared (bit-identical to separate rot calls)."""
+        k = len(offsets)
+        hs = (ctypes.c_void_p * k)(*[o.h for o in outs])
+        ol = (ctypes.c_uint32 * k)(*(out_lanes or [0] * k))
+        of = (ctypes.c_int * k)(*offsets)
+        self._call("aegis_rot_hoisted", hs, ol, of, k, inp.h, in_lane, inp.lanes if lanes is None else lanes, level)
+
+    def limb_op(self, opcode, out, a=None, b=None, lo=0, hi=None, lanes=None, out_lane=0, a_slice=None,
+                b_slice=None, param=0):
+        """kLimbMulAdd with LimbOpcode `opcode` (_lib.LIMB_*) on limbs [lo, hi] (poly_ir.hpp:49-58, 192-213)."""
+        lanes = out.lanes if lanes is None else lanes
+        al, ac = a_slice or ((0, a.lanes) if a is not None else (0, 0))
+        bl, bc = b_slice or ((0, b.lanes) if b is not None else (0, 0))
+        self._call("aegis_limb_op", opcode, out.h, out_lane, lanes, a.h if a is not None else None, al, ac,
+                   b.h if b is not None else None, bl, bc, lo, out.level - 1 if hi is None else hi, param)
+
+    def limb_drop(self, out, inp, level, mode=0, out_lane=0, in_lane=0, lanes=None):
+        """kLimbDrop (poly_ir.hpp:341-354): mode 0 truncates, 3 (kRescaleTail) rescales."""
+        self._call("aegis_limb_drop", out.h, out_lane, inp.h, in_lane, inp.lanes if lanes is None else lanes,
+                   level, mode)
+
+    def padd(self, out, ct, pt, level, lanes=None, ct_slice=None, pt_slice=None, out_lane=0):
+        lanes = out.lanes if lanes is None else lanes
+        cl, cc = ct_slice or (0, ct.lanes)
+        pl, pc = pt_slice or (0, pt.lanes)
+        self._call("aegis_padd", out.h, out_lane, lanes, ct.h, cl, cc, pt.h, pl, pc, level)
+
+    def encode(self, pt, weight_bundle, level, lane=0, lanes=None):
+        """kEncode: the kGenerate weights of bundle id `weight_bundle` into a 1-component bundle."""
+        self._call("aegis_encode", pt.h, lane, pt.lanes if lanes is None else lanes, level, weight_bundle)
+
     def relin(self, b, level, lane=0, lanes=None):
         self._call("aegis_relin", b.h, lane, b.lanes if lanes is None else lanes, level)
 
@@ -241,6 +273,27 @@ class Context:
         self._call("aegis_graph_load", str(path).encode(), ctypes.byref(h))
         return Graph(self.lib, h, self)
 
+    def graph_from_ops(self, meta, bundles, ops, inputs):
+        """In-memory HeOpGraph ingest (aegis_graph_from_ops): see graph_from_ops()."""
+        g = graph_from_ops(meta, bundles, ops, inputs)
+        g.ctx = self
+        return g
+
+
+def graph_from_ops(meta, bundles, ops, inputs):
+    """Build a graph from descriptor arrays (_lib.AegisGraphMeta, AegisBundleDesc[],
+    AegisOpDesc[], bundle ids) with no text round trip; no device needed."""
+    lib = L.load()
+    nb, no, ni = len(bundles), len(ops), len(inputs)
+    barr = (L.AegisBundleDesc * max(nb, 1))(*bundles)
+    oarr = (L.AegisOpDesc * max(no, 1))(*ops)
+    iarr = (ctypes.c_uint32 * max(ni, 1))(*inputs)
+    h = ctypes.c_void_p()
+    rc = lib.aegis_graph_from_ops(ctypes.byref(meta), barr, nb, oarr, no, iarr, ni, ctypes.byref(h))
+    if rc != L.AEGIS_OK:
+        _raise(rc, lib.aegis_last_error(None).decode())
+    return Graph(lib, h, None)
+
 
 def plan_graph(log_n=16, chain_length=35, bootstrap_level=14, kind=0, tokens=128, layers=1,
                model_dim=768, ffn_dim=3072, head_dim=64, slots_per_token=64):
@@ -263,6 +316,20 @@ class Graph:
         o, b = ctypes.c_uint64(), ctypes.c_uint64()
         self.lib.aegis_graph_info(self.h, ctypes.byref(o), ctypes.byref(b))
         return o.value, b.value
+
+    def export(self):
+        """-> (meta, [AegisBundleDesc], [AegisOpDesc], [input bundle ids]) (aegis_graph_export)."""
+        nops, nb = self.info()
+        ni = ctypes.c_uint32()
+        self.lib.aegis_graph_export(self.h, None, 0, None, 0, None, 0, ctypes.byref(ni), None)
+        barr = (L.AegisBundleDesc * max(nb, 1))()
+        oarr = (L.AegisOpDesc * max(nops, 1))()
+        iarr = (ctypes.c_uint32 * max(ni.value, 1))()
+        meta = L.AegisGraphMeta()
+        rc = self.lib.aegis_graph_export(self.h, barr, nb, oarr, nops, iarr, ni.value, None, ctypes.byref(meta))
+        if rc:
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+        return meta, list(barr)[:nb], list(oarr)[:nops], list(iarr)[:ni.value]
 
     def dump(self, path):
         rc = self.lib.aegis_graph_dump(self.h, str(path).encode())

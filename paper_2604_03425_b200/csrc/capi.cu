@@ -392,6 +392,141 @@ int aegis_rot(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_
     ctx->c->op_rot(o, out_lane, i, LaneMap{in_lane, lanes}, lanes, level, offset);
   });
 }
+int aegis_rot_hoisted(aegis_ctx* ctx, aegis_bundle* const* outs, const uint32_t* out_lanes, const int* offsets,
+                      uint32_t n_off, const aegis_bundle* in, uint32_t in_lane, uint32_t lanes, uint32_t level) {
+  return guard(ctx, [&] {
+    const Bundle& i = need(in);
+    if (!n_off) return;
+    if (!outs || !out_lanes || !offsets) throw Error(AEGIS_EINVAL, "rot_hoisted: null argument");
+    check_lanes(i, in_lane, lanes, "rot_hoisted");
+    check_level(i, level, "rot_hoisted");
+    if (i.comps < 2) throw Error(AEGIS_EINVAL, "rot_hoisted: the source must be a ciphertext");
+    for (u32 k = 0; k < n_off; ++k) {
+      Bundle& o = need(outs[k]);
+      check_lanes(o, out_lanes[k], lanes, "rot_hoisted");
+      check_level(o, level, "rot_hoisted");
+      if (o.comps < 2) throw Error(AEGIS_EINVAL, "rot_hoisted: outputs must have 2 components");
+      if (&o == &i && out_lanes[k] < in_lane + lanes && in_lane < out_lanes[k] + lanes)
+        throw Error(AEGIS_EINVAL, "rot_hoisted: output lanes overlap the input lanes");
+      Context::rotation_key_id(offsets[k]);  // offset range check before any work
+    }
+    Context& c = *ctx->c;
+    // ModUp(c1) once per lane batch, shared by every offset (bit-identical to
+    // the per-rotation ModUp: the key is pre-permuted)
+    const size_t per_lane = c.modup_words_per_lane(level);
+    const u32 batch = (u32)std::max<size_t>(1, std::min<size_t>(lanes, c.ws_budget(2) / (per_lane * 8)));
+    u64* ext = c.alloc(per_lane * batch);
+    try {
+      const size_t in_ls = (size_t)i.comps * i.level * c.n;
+      for (u32 done = 0; done < lanes; done += batch) {
+        const u32 cnt = std::min(batch, lanes - done);
+        c.modup(i.view().limb(in_lane + done, 1, 0, c.n), in_ls, cnt, level, ext);
+        for (u32 k = 0; k < n_off; ++k)
+          c.op_rot_cached(*outs[k]->b, out_lanes[k] + done, i, LaneMap{in_lane + done, cnt}, cnt, level,
+                          offsets[k], ext);
+      }
+    } catch (...) {
+      c.release(ext);
+      throw;
+    }
+    c.release(ext);
+  });
+}
+int aegis_padd(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, uint32_t lanes, const aegis_bundle* ct,
+               uint32_t ct_lane, uint32_t ct_count, const aegis_bundle* pt, uint32_t pt_lane, uint32_t pt_count,
+               uint32_t level) {
+  return guard(ctx, [&] {
+    const Bundle& P = need(pt);
+    const Bundle& C = need(ct);
+    if (P.comps != 1) throw Error(AEGIS_EINVAL, "padd: the plaintext operand must have 1 component");
+    if (C.comps < 2) throw Error(AEGIS_EINVAL, "padd: the ciphertext operand must have 2 components");
+    if (level == 0) throw Error(AEGIS_EINVAL, "exhausted modulus chain");
+    const int rc = aegis_limb_op(ctx, AEGIS_LIMB_ADD, out, out_lane, lanes, ct, ct_lane, ct_count, pt, pt_lane,
+                                 pt_count, 0, level - 1, 0);
+    if (rc) throw Error(rc, ctx->err);
+  });
+}
+int aegis_encode(aegis_ctx* ctx, aegis_bundle* pt, uint32_t lane, uint32_t lanes, uint32_t level, uint32_t wb) {
+  return guard(ctx, [&] {
+    Bundle& P = need(pt);
+    check_lanes(P, lane, lanes, "encode");
+    check_level(P, level, "encode");
+    if (P.comps != 1) throw Error(AEGIS_EINVAL, "encode: plaintext bundles have 1 component");
+    Context& c = *ctx->c;
+    AEGIS_CHECK_CUDA(aegis::launch_limb_generate(P.view(), lane, lanes, 1, 0, level, c.n, c.seed_weight, 2, wb, c.d_pc,
+                                                 c.stream));
+    c.count();
+  });
+}
+int aegis_limb_op(aegis_ctx* ctx, int opcode, aegis_bundle* out, uint32_t out_lane, uint32_t lanes,
+                  const aegis_bundle* a, uint32_t a_lane, uint32_t a_count, const aegis_bundle* b, uint32_t b_lane,
+                  uint32_t b_count, uint32_t lo, uint32_t hi, uint64_t param) {
+  return guard(ctx, [&] {
+    Bundle& o = need(out);
+    Context& c = *ctx->c;
+    check_lanes(o, out_lane, lanes, "limb_op");
+    if (lo > hi || hi >= o.level) throw Error(AEGIS_EINVAL, "limb_op: prime range outside the output's limbs");
+    const u32 limbs = hi - lo + 1;
+    if (opcode == AEGIS_LIMB_KEYMUL)
+      throw Error(AEGIS_EINVAL, "limb_op: kKeyMul runs inside aegis_keyswitch (the IR's KeyMul has no digit split)");
+    if (opcode == AEGIS_LIMB_GENERATE) {
+      AEGIS_CHECK_CUDA(aegis::launch_limb_generate(o.view(), out_lane, lanes, o.comps, lo, limbs, c.n, c.seed_weight,
+                                                   2, param, c.d_pc, c.stream));
+      c.count();
+      return;
+    }
+    if (opcode < AEGIS_LIMB_ADD || opcode > AEGIS_LIMB_ADDACC) throw Error(AEGIS_EINVAL, "limb_op: unknown opcode");
+    const Bundle& A = need(a);
+    check_lanes(A, a_lane, a_count, "limb_op");
+    if (!a_count) throw Error(AEGIS_EINVAL, "limb_op: empty operand");
+    if (hi >= A.level) throw Error(AEGIS_EINVAL, "limb_op: prime range outside an operand's limbs");
+    const bool two = opcode != AEGIS_LIMB_ADDACC;
+    const Bundle* B = nullptr;
+    if (two) {
+      B = &need(b);
+      check_lanes(*B, b_lane, b_count, "limb_op");
+      if (!b_count) throw Error(AEGIS_EINVAL, "limb_op: empty operand");
+      if (hi >= B->level) throw Error(AEGIS_EINVAL, "limb_op: prime range outside an operand's limbs");
+    }
+    const u32 ac = std::min<u32>(A.comps, 2), bc = B ? std::min<u32>(B->comps, 2) : 0;
+    if (A.comps > 2 || (B && B->comps > 2)) throw Error(AEGIS_EINVAL, "limb_op: operands have at most 2 components");
+    const bool mul = opcode == AEGIS_LIMB_MUL || opcode == AEGIS_LIMB_MULACC;
+    const u32 oc = opcode == AEGIS_LIMB_ADDACC ? o.comps : (mul && ac == 2 && bc == 2 ? 3 : std::max(ac, bc));
+    if (oc > o.comps) throw Error(AEGIS_EINVAL, "limb_op: the output has too few components");
+    auto overlaps = [&](const Bundle& X, u32 xl, u32 xc) {
+      return &X == &o && xl < out_lane + lanes && out_lane < xl + xc && !(xl == out_lane && xc == lanes);
+    };
+    if (overlaps(A, a_lane, a_count) || (B && overlaps(*B, b_lane, b_count)))
+      throw Error(AEGIS_EINVAL, "limb_op: the output overlaps an operand with different lanes");
+    const aegis::View bv = B ? B->view() : A.view();
+    AEGIS_CHECK_CUDA(aegis::launch_limb_op(opcode, o.view(), out_lane, oc, A.view(), LaneMap{a_lane, a_count}, ac, bv,
+                                           LaneMap{b_lane, b_count ? b_count : 1}, bc, lanes, lo, limbs, c.n, c.d_pc,
+                                           c.stream));
+    c.count();
+  });
+}
+int aegis_limb_drop(aegis_ctx* ctx, aegis_bundle* out, uint32_t out_lane, const aegis_bundle* in, uint32_t in_lane,
+                    uint32_t lanes, uint32_t level, int mode) {
+  if (mode == AEGIS_MODE_RESCALE_TAIL) return aegis_rescale(ctx, out, out_lane, in, in_lane, lanes, level);
+  return guard(ctx, [&] {
+    if (mode != AEGIS_MODE_NONE) throw Error(AEGIS_EINVAL, "limb_drop: mode must be kNone or kRescaleTail");
+    Bundle& o = need(out);
+    const Bundle& i = need(in);
+    check_lanes(o, out_lane, lanes, "limb_drop");
+    check_lanes(i, in_lane, lanes, "limb_drop");
+    check_level(i, level, "limb_drop");
+    if (level < 2) throw Error(AEGIS_EINVAL, "level underflow: cannot drop below level 1");
+    check_level(o, level - 1, "limb_drop");
+    if (o.comps < i.comps) throw Error(AEGIS_EINVAL, "limb_drop: the output has too few components");
+    if (&o == &i && in_lane == out_lane) return;  // the dropped limb is simply no longer read
+    if (&o == &i && out_lane < in_lane + lanes && in_lane < out_lane + lanes)
+      throw Error(AEGIS_EINVAL, "limb_drop: output lanes overlap the input lanes");
+    Context& c = *ctx->c;
+    AEGIS_CHECK_CUDA(aegis::launch_copy(o.view(), out_lane, i.view(), LaneMap{in_lane, lanes}, lanes, i.comps,
+                                        level - 1, 0, c.n, c.stream));
+    c.count();
+  });
+}
 int aegis_relin(aegis_ctx* ctx, aegis_bundle* b, uint32_t lane, uint32_t lanes, uint32_t level) {
   return guard(ctx, [&] {
     Bundle& bb = need(b);
@@ -555,6 +690,122 @@ int aegis_graph_info(const aegis_graph* g, uint64_t* ops, uint64_t* bundles) {
   if (ops) *ops = g->g.ops.size();
   if (bundles) *bundles = g->g.bundles.size();
   return AEGIS_OK;
+}
+namespace {
+std::string header_of(const aegis_graph_meta& m) {
+  std::ostringstream h;
+  h << "# heops v1 N=" << (1u << m.log_n) << " L=" << m.chain_length << " K=" << aegis::kAlpha
+    << " lboot=" << m.bootstrap_level << " stok=" << m.slots_per_token << " d=" << m.model_dim
+    << " hd=" << m.head_dim << " dff=" << m.ffn_dim << " T=" << m.tokens << " layers=" << m.layers
+    << " kind=" << m.kind << " exact=0";
+  return h.str();
+}
+}  // namespace
+int aegis_graph_from_ops(const aegis_graph_meta* meta, const aegis_bundle_desc* bundles, uint32_t nb,
+                         const aegis_op_desc* ops, uint64_t nops, const uint32_t* inputs, uint32_t ninputs,
+                         aegis_graph** out) {
+  return guard(nullptr, [&] {
+    if (!meta || !out || (nb && !bundles) || (nops && !ops) || (ninputs && !inputs))
+      throw Error(AEGIS_EINVAL, "graph_from_ops: null argument");
+    if (meta->log_n < 4 || meta->log_n > AEGIS_MAX_LOG_N) throw Error(AEGIS_EINVAL, "ring_degree must be a power of two");
+    if (!meta->slots_per_token) throw Error(AEGIS_EINVAL, "layout dimensions must be positive");
+    auto g = std::make_unique<aegis_graph>();
+    g->g.bundles.reserve(nb);
+    for (uint32_t i = 0; i < nb; ++i) {
+      const aegis_bundle_desc& d = bundles[i];
+      hp::CtBundle b;
+      b.id = i;
+      b.lanes = d.lanes;
+      b.level = d.level;
+      b.components = d.components;
+      if (d.cls > (uint32_t)hp::BundleClass::kScore || d.aggregation > (uint32_t)hp::AggregationAxis::kHeadWise)
+        throw Error(AEGIS_EINVAL, "graph_from_ops: bundle " + std::to_string(i) + " has an unknown class");
+      b.cls = (hp::BundleClass)d.cls;
+      b.aggregation = (hp::AggregationAxis)d.aggregation;
+      b.app_node = d.app_node;
+      b.chunk_period = d.chunk_period;
+      b.replicate_hint = d.replicate_hint != 0;
+      if (d.tag) b.tag = d.tag;
+      g->g.bundles.push_back(std::move(b));
+    }
+    g->g.ops.reserve(nops);
+    for (uint64_t i = 0; i < nops; ++i) {
+      const aegis_op_desc& d = ops[i];
+      if (d.in_count > AEGIS_MAX_OP_INPUTS) throw Error(AEGIS_EINVAL, "heops: op " + std::to_string(i) + ": too many operands");
+      if (d.kind > (uint32_t)hp::HeOpKind::kBoot) throw Error(AEGIS_EINVAL, "heops: op " + std::to_string(i) + ": unknown kind");
+      hp::HeOp op;
+      op.id = (uint32_t)i;
+      op.kind = (hp::HeOpKind)d.kind;
+      op.rot_offset = d.rot_offset;
+      op.out = hp::LaneSlice{d.out.bundle, d.out.lane, d.out.lane_count};
+      for (uint32_t k = 0; k < d.in_count; ++k) op.ins.push_back(hp::LaneSlice{d.ins[k].bundle, d.ins[k].lane, d.ins[k].lane_count});
+      op.accumulate = d.accumulate != 0;
+      op.aligned = d.aligned != 0;
+      op.phase = d.phase;
+      op.work = d.work;
+      op.use_level = d.use_level;
+      op.app_node = d.app_node;
+      if (d.aggregation > (uint32_t)hp::AggregationAxis::kHeadWise)
+        throw Error(AEGIS_EINVAL, "heops: op " + std::to_string(i) + ": unknown aggregation axis");
+      op.aggregation = (hp::AggregationAxis)d.aggregation;
+      g->g.ops.push_back(std::move(op));
+    }
+    g->g.graph_inputs.assign(inputs, inputs + ninputs);
+    hp::validate_heops(g->g);
+    g->header = header_of(*meta);
+    *out = g.release();
+  });
+}
+int aegis_graph_export(const aegis_graph* g, aegis_bundle_desc* bundles, uint32_t bcap, aegis_op_desc* ops,
+                       uint64_t ocap, uint32_t* inputs, uint32_t icap, uint32_t* n_inputs, aegis_graph_meta* meta) {
+  return guard(nullptr, [&] {
+    if (!g) throw Error(AEGIS_EINVAL, "null graph");
+    if ((bundles && bcap < g->g.bundles.size()) || (ops && ocap < g->g.ops.size()) ||
+        (inputs && icap < g->g.graph_inputs.size()))
+      throw Error(AEGIS_EINVAL, "graph_export: buffer too small");
+    if (bundles)
+      for (size_t i = 0; i < g->g.bundles.size(); ++i) {
+        const hp::CtBundle& b = g->g.bundles[i];
+        bundles[i] = aegis_bundle_desc{b.lanes, b.level, b.components, (uint32_t)b.cls, (uint32_t)b.aggregation,
+                                       b.app_node, b.chunk_period, (uint32_t)b.replicate_hint, b.tag.c_str()};
+      }
+    if (ops)
+      for (size_t i = 0; i < g->g.ops.size(); ++i) {
+        const hp::HeOp& op = g->g.ops[i];
+        if (op.ins.size() > AEGIS_MAX_OP_INPUTS) throw Error(AEGIS_EINVAL, "graph_export: op with too many operands");
+        aegis_op_desc d{};
+        d.kind = (uint32_t)op.kind;
+        d.accumulate = op.accumulate;
+        d.aligned = op.aligned;
+        d.aggregation = (uint32_t)op.aggregation;
+        d.rot_offset = op.rot_offset;
+        d.phase = op.phase;
+        d.out = aegis_slice{op.out.bundle, op.out.lane, op.out.lane_count};
+        d.in_count = (uint32_t)op.ins.size();
+        for (size_t k = 0; k < op.ins.size(); ++k) d.ins[k] = aegis_slice{op.ins[k].bundle, op.ins[k].lane, op.ins[k].lane_count};
+        d.work = op.work;
+        d.use_level = op.use_level;
+        d.app_node = op.app_node;
+        ops[i] = d;
+      }
+    if (inputs) std::copy(g->g.graph_inputs.begin(), g->g.graph_inputs.end(), inputs);
+    if (n_inputs) *n_inputs = (uint32_t)g->g.graph_inputs.size();
+    if (meta) {
+      const uint64_t n = header_value(g->header, "N");
+      aegis_graph_meta m{};
+      while ((1ull << m.log_n) < n) ++m.log_n;
+      m.chain_length = (uint32_t)header_value(g->header, "L");
+      m.bootstrap_level = (uint32_t)header_value(g->header, "lboot");
+      m.slots_per_token = (uint32_t)header_value(g->header, "stok");
+      m.model_dim = (uint32_t)header_value(g->header, "d");
+      m.head_dim = (uint32_t)header_value(g->header, "hd");
+      m.ffn_dim = (uint32_t)header_value(g->header, "dff");
+      m.layers = (uint32_t)header_value(g->header, "layers");
+      m.kind = (uint32_t)header_value(g->header, "kind");
+      m.tokens = header_value(g->header, "T");
+      *meta = m;
+    }
+  });
 }
 int aegis_graph_set_shard(aegis_graph* g, uint32_t world, uint32_t rank) {
   if (!g) return AEGIS_EINVAL;

@@ -138,4 +138,13 @@ cudaError_t launch_hash(View v, u32 lane0, u32 lanes, u32 comps, u32 limbs, u32 
 cudaError_t launch_reduce_lanes(View v, u32 lane0, u32 lanes, u32 comps, u32 limbs, u32 n, const PrimeConst* pc,
                                 cudaStream_t st);
 
+// pointwise limb instruction (limb_ops.cu; opcode = LimbOpcode, poly_ir.hpp:49-58) over
+// lanes x limbs [limb_lo, limb_lo + limbs) of every output component
+cudaError_t launch_limb_op(int opcode, View out, u32 out_lane0, u32 out_comps, View a, LaneMap ma, u32 a_comps,
+                           View b, LaneMap mb, u32 b_comps, u32 nlanes, u32 limb_lo, u32 limbs, u32 n,
+                           const PrimeConst* pc, cudaStream_t st);
+// kGenerate rows keyed by (seed, tag, bundle, absolute lane, comp, absolute limb)
+cudaError_t launch_limb_generate(View out, u32 out_lane0, u32 nlanes, u32 comps, u32 limb_lo, u32 limbs, u32 n,
+                                 u64 seed, u64 tag, u64 bundle, const PrimeConst* pc, cudaStream_t st);
+
 }  // namespace aegis

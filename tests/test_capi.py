@@ -91,3 +91,42 @@ def test_graph_load_validates_every_index(tmp_path, golden_dir):
     mutate(6, 1 << 20, "output lane count beyond the bundle")
     mutate(11, 60, "use_level above the operand level")
     mutate(3, -700, "rotation offset aliasing the relin key ids")
+
+
+def test_graph_from_ops_round_trip(tmp_path):
+    """In-memory HeOpGraph ingest (aegis_graph_from_ops): exporting a lowered
+    graph to descriptor arrays and ingesting them back gives the identical
+    graph (same heops dump), with no text round trip and no device."""
+    from paper_2604_03425_b200 import plan_graph
+    from paper_2604_03425_b200.api import graph_from_ops
+    for kind, tokens in ((1, 128), (0, 512)):
+        g = plan_graph(log_n=16, kind=kind, tokens=tokens)
+        meta, bundles, ops, inputs = g.export()
+        assert meta.log_n == 16 and meta.tokens == tokens and meta.kind == kind
+        h = graph_from_ops(meta, bundles, ops, inputs)
+        a, b = tmp_path / "a.heops", tmp_path / "b.heops"
+        g.dump(a)
+        h.dump(b)
+        assert open(a).read() == open(b).read()
+        assert h.key_ids().tolist() == g.key_ids().tolist()
+
+
+def test_graph_from_ops_validates(tmp_path):
+    from paper_2604_03425_b200 import plan_graph
+    from paper_2604_03425_b200.api import graph_from_ops
+    g = plan_graph(log_n=16, kind=1, tokens=128)
+    meta, bundles, ops, inputs = g.export()
+    rot = next(i for i, o in enumerate(ops) if o.kind == 5)
+    cases = [("bundle", lambda o: setattr(o.out, "bundle", len(bundles) + 3), "outside its bundle"),
+             ("lane", lambda o: setattr(o.ins[0], "lane_count", 10_000), "outside its bundle"),
+             ("level", lambda o: setattr(o, "use_level", 60), "use_level"),
+             ("offset", lambda o: setattr(o, "rot_offset", -700), "offset"),
+             ("kind", lambda o: setattr(o, "kind", 42), "unknown kind"),
+             ("ins", lambda o: setattr(o, "in_count", 9), "too many operands")]
+    for name, mutate, msg in cases:
+        bad = list(ops)
+        o = type(ops[rot]).from_buffer_copy(ops[rot])
+        mutate(o)
+        bad[rot] = o
+        with pytest.raises(ValueError, match=msg):
+            graph_from_ops(meta, bundles, bad, inputs)
