@@ -103,6 +103,20 @@ int aegis_keys_generate(aegis_ctx* ctx, const uint64_t* key_ids, uint32_t count)
 int aegis_keys_upload(aegis_ctx* ctx, uint64_t key_id, const uint64_t* host, uint64_t words, int coeff_domain);
 int aegis_keys_bytes(const aegis_ctx* ctx, uint64_t* out);
 
+/* ---- wire / disk format (csrc/store.cu) --------------
+ * 128-byte header (magic "AEGS", ring, prime-chain fingerprint, shape, key id,
+ * DESIGN.md §2.4 content hash) + little-endian u64 payload.  Bundles are
+ * [lane][comp][limb][N] (encoded plaintexts are 1-component bundles, e.g. the
+ * weights aegis_encode writes; ckks.hpp:226-283 byte model); keys are the
+ * library's internal [digit][comp][slot][N] form (rotation keys
+ * pre-permuted).  Transfers stream through two pinned 64 MiB buffers so file
+ * I/O overlaps the DMA; a load recomputes the content hash on the device and
+ * rejects torn, foreign-chain or mismatched files with EINVAL. */
+int aegis_bundle_save(aegis_ctx* ctx, const aegis_bundle* b, const char* path);
+int aegis_bundle_load(aegis_ctx* ctx, const char* path, aegis_bundle** out);
+int aegis_keys_save(aegis_ctx* ctx, uint64_t key_id, const char* path);
+int aegis_keys_load(aegis_ctx* ctx, uint64_t key_id, const char* path);
+
 /* ---- polynomial instructions (PolyOpKind, poly_ir.hpp:23-32) -------------
  * FragSpan-style addressing (poly_ir.hpp:87-99): lanes [lane, lane+lane_count)
  * and limbs [prime_lo, prime_hi] of every component of bundle b.          */
@@ -200,6 +214,14 @@ int aegis_pmult_acc(aegis_ctx* ctx, aegis_bundle* acc, uint32_t acc_lane, uint32
                     uint32_t chunk_period, const aegis_bundle* x, uint32_t x_lane, uint32_t x_lanes,
                     uint32_t weight_bundle_id, uint32_t weight_lanes, uint32_t level);
 
+/* the same PCMM step with STORED plaintext weights (SURVEY §8(d) stored
+ * variant; ckks.hpp:226-283 plaintext bytes): lanes [w_lane, w_lane + w_lanes)
+ * of the 1-component bundle w hold W[ci * c_out + o] (e.g. written by
+ * aegis_encode or aegis_bundle_load); the kernel streams them from HBM. */
+int aegis_pmult_acc_stored(aegis_ctx* ctx, aegis_bundle* acc, uint32_t acc_lane, uint32_t acc_lanes,
+                           uint32_t chunk_period, const aegis_bundle* x, uint32_t x_lane, uint32_t x_lanes,
+                           const aegis_bundle* w, uint32_t w_lane, uint32_t w_lanes, uint32_t level);
+
 /* ---- layer drivers + executor (he_ir.hpp:683 lower_app_to_he; SPEC exec_*) */
 typedef struct aegis_model {
   uint32_t kind;        /* 0: transformer blocks (graph.hpp:168), 1: FFN only (config 1) */
@@ -278,9 +300,75 @@ int aegis_graph_set_reducer(aegis_graph* g, aegis_reduce_fn fn, void* user);
  * share `part` (the reduce hook's semantics). */
 int aegis_p2p_create(aegis_ctx* ctx, uint64_t bytes, void* handle_out, aegis_p2p** out);
 int aegis_p2p_open(aegis_ctx* ctx, aegis_p2p* w, const void* handles, uint32_t m, uint32_t self);
+/* same-process group (one host thread per context, or one thread driving
+ * several contexts): group[r] is rank r's window, used through its device
+ * pointer (no IPC mapping) */
+int aegis_p2p_open_local(aegis_ctx* ctx, aegis_p2p* w, aegis_p2p* const* group, uint32_t m, uint32_t self);
 int aegis_p2p_stage(aegis_ctx* ctx, aegis_p2p* w, const uint64_t* buf, uint64_t words);
 int aegis_p2p_reduce(aegis_ctx* ctx, aegis_p2p* w, uint64_t* dst, uint64_t words_per_rank, uint32_t part);
 int aegis_p2p_destroy(aegis_p2p* w);
+/* The executor's own data plane for the sharded PCMM reduce-scatter (the
+ * comm stream of PAPER.md:518 / comm_plan.hpp:88-91): with a window attached,
+ * aegis_graph_run needs no reduce hook.  As soon as the last PMult of an
+ * accumulator is issued, every sub-tensor is exchanged on aegis_stream_comm
+ * -- pushes into the peers' windows, flags in peer memory, sums, acks -- and
+ * the compute stream waits on a CUDA event only when an op touches those
+ * lanes, so the rescale of one sub-tensor overlaps the exchange of the next.
+ * No host barrier or callback runs inside the layer.  aegis_graph_p2p_bytes
+ * gives the window size the current shard needs (call after set_shard; 0
+ * when no token group spans several ranks).  The window must stay alive while
+ * the graph runs; every rank of a group must attach windows of equal size. */
+int aegis_graph_p2p_bytes(const aegis_graph* g, uint64_t* bytes);
+int aegis_graph_set_p2p(aegis_graph* g, aegis_p2p* w);
+/* stored-plaintext PCMM for the whole graph (separately reported variant):
+ * every kEncode op writes its weight bundle to HBM and each PMult reads it
+ * (aegis_pmult_acc_stored) instead of generating the weights in-kernel.  All
+ * ciphertext bundles are bit-identical to the default; weight bundles are not
+ * hashed.  Default off. */
+int aegis_graph_set_stored_weights(aegis_graph* g, int enable);
+/* fault injection for tests: kind 1 drops the PCMM exchange (every rank keeps
+ * its partial sums); 0 restores normal execution */
+int aegis_graph_set_fault(aegis_graph* g, int kind);
+/* ---- execution plan (comm_plan.hpp:51-118 ExecutionPlan; plan.h) ---------
+ * The Aegis plan of this graph on `world` devices under token-coherent
+ * placement: per device the compute instructions (HeOp, owned lane run,
+ * flags, the event it waits for) and the collective events (kind, semantic,
+ * participants, payload, bytes, trigger/wait positions), plus, per matmul,
+ * the bytes of both collective modes and the one the reference's rule picks
+ * (comm_plan.hpp:226-238) next to the one this executor runs.  reorder
+ * staggers the rotation-offset order per device part.  If the
+ * shape cannot be split over `world` devices the plan has executable = 0, no
+ * devices or events, and still the matmul analysis.  No device needed. */
+typedef struct aegis_plan aegis_plan;
+typedef struct aegis_plan_summary {
+  uint32_t world, token_groups, ranks_per_group, reordered, executable, matmuls, matmuls_gather_chosen, pad;
+  uint64_t events, events_executed, instrs_total;
+  uint64_t bytes_total, bytes_ffn, bytes_attention, bytes_layernorm, bytes_boot, bytes_other;
+  uint64_t bytes_reference_rule; /* total if every matmul used the mode the reference's rule picks */
+} aegis_plan_summary;
+typedef struct aegis_plan_event {
+  uint32_t id, kind /* 0 AllGather, 1 ReduceScatter, 2 AllReduce */, semantic /* 0 Move, 1 Combine, 2 CombineScatter */;
+  uint32_t dev_lo, dev_count, bundle, lane, lane_count, level, category, app_node, he_op, executed;
+  uint64_t bytes_per_device, bytes_total;
+} aegis_plan_event;
+typedef struct aegis_plan_instr {
+  uint32_t op, lane, lane_count, flags;
+  int32_t wait_event;
+} aegis_plan_instr;
+typedef struct aegis_plan_matmul {
+  uint32_t app_node, acc_bundle, input_bundle, ship_bundle, chosen, executed; /* 0 local, 1 gather, 2 reduce */
+  uint64_t gather_bytes, reduce_bytes;
+} aegis_plan_matmul;
+int aegis_plan_build(const aegis_graph* g, uint32_t world, int reorder, aegis_plan** out);
+int aegis_plan_summary_get(const aegis_plan* p, aegis_plan_summary* out);
+int aegis_plan_events(const aegis_plan* p, aegis_plan_event* out, uint64_t cap, uint64_t* n);
+int aegis_plan_device(const aegis_plan* p, uint32_t device, aegis_plan_instr* out, uint64_t cap, uint64_t* n);
+int aegis_plan_matmuls(const aegis_plan* p, aegis_plan_matmul* out, uint64_t cap, uint64_t* n);
+const char* aegis_plan_note(const aegis_plan* p);
+int aegis_plan_free(aegis_plan* p);
+/* bytes this rank sent through its PCMM exchanges in the last aegis_graph_run
+ * (the executed counterpart of the plan's events) */
+int aegis_graph_comm_bytes(const aegis_graph* g, uint64_t* bytes);
 /* lane ownership of bundle `bundle` under the current shard (1 = owned) */
 int aegis_graph_owned_lanes(const aegis_graph* g, uint32_t bundle, uint8_t* mask, uint32_t cap);
 int aegis_graph_shard_info(const aegis_graph* g, uint32_t* tg_total, uint32_t* tg_lo, uint32_t* tg_hi,

@@ -57,6 +57,29 @@ class AegisOpDesc(ctypes.Structure):
                 ("app_node", u32)]
 
 
+class AegisPlanSummary(ctypes.Structure):
+    _fields_ = [(f, u32) for f in ("world", "token_groups", "ranks_per_group", "reordered", "executable", "matmuls",
+                                   "matmuls_gather_chosen", "pad")] + \
+               [(f, u64) for f in ("events", "events_executed", "instrs_total", "bytes_total", "bytes_ffn",
+                                   "bytes_attention", "bytes_layernorm", "bytes_boot", "bytes_other",
+                                   "bytes_reference_rule")]
+
+
+class AegisPlanEvent(ctypes.Structure):
+    _fields_ = [(f, u32) for f in ("id", "kind", "semantic", "dev_lo", "dev_count", "bundle", "lane", "lane_count",
+                                   "level", "category", "app_node", "he_op", "executed")] + \
+               [("bytes_per_device", u64), ("bytes_total", u64)]
+
+
+class AegisPlanInstr(ctypes.Structure):
+    _fields_ = [("op", u32), ("lane", u32), ("lane_count", u32), ("flags", u32), ("wait_event", ctypes.c_int32)]
+
+
+class AegisPlanMatmul(ctypes.Structure):
+    _fields_ = [(f, u32) for f in ("app_node", "acc_bundle", "input_bundle", "ship_bundle", "chosen", "executed")] + \
+               [("gather_bytes", u64), ("reduce_bytes", u64)]
+
+
 # LimbOpcode (poly_ir.hpp:49-58) and PolyMode (:60-65) values of the C-ABI
 LIMB_ADD, LIMB_SUB, LIMB_MUL, LIMB_MULACC, LIMB_ADDACC, LIMB_KEYMUL, LIMB_GENERATE = range(1, 8)
 MODE_NONE, MODE_KEY_SWITCH, MODE_BOOT_RESET, MODE_RESCALE_TAIL = range(4)
@@ -84,6 +107,10 @@ SIGNATURES = [
     ("aegis_keys_generate", ctypes.c_int, [vp, u64p, u32]),
     ("aegis_keys_upload", ctypes.c_int, [vp, u64, u64p, u64, ctypes.c_int]),
     ("aegis_keys_bytes", ctypes.c_int, [vp, u64p]),
+    ("aegis_bundle_save", ctypes.c_int, [vp, vp, ctypes.c_char_p]),
+    ("aegis_bundle_load", ctypes.c_int, [vp, ctypes.c_char_p, ctypes.POINTER(vp)]),
+    ("aegis_keys_save", ctypes.c_int, [vp, u64, ctypes.c_char_p]),
+    ("aegis_keys_load", ctypes.c_int, [vp, u64, ctypes.c_char_p]),
     ("aegis_ntt", ctypes.c_int, [vp, vp, u32, u32, u32, u32, ctypes.c_int]),
     ("aegis_automorphism", ctypes.c_int, [vp, vp, vp, u32, u32, u32, u64]),
     ("aegis_basis_convert", ctypes.c_int, [vp, vp, vp, u32p, u32p, u32, u32p, u32p, u32]),
@@ -116,6 +143,14 @@ SIGNATURES = [
     ("aegis_graph_set_shard", ctypes.c_int, [vp, u32, u32]),
     ("aegis_graph_set_hash_group", ctypes.c_int, [vp, ctypes.c_int32]),
     ("aegis_graph_set_reducer", ctypes.c_int, [vp, vp, vp]),
+    ("aegis_plan_build", ctypes.c_int, [vp, u32, ctypes.c_int, ctypes.POINTER(vp)]),
+    ("aegis_plan_summary_get", ctypes.c_int, [vp, ctypes.POINTER(AegisPlanSummary)]),
+    ("aegis_plan_events", ctypes.c_int, [vp, ctypes.POINTER(AegisPlanEvent), u64, u64p]),
+    ("aegis_plan_device", ctypes.c_int, [vp, u32, ctypes.POINTER(AegisPlanInstr), u64, u64p]),
+    ("aegis_plan_matmuls", ctypes.c_int, [vp, ctypes.POINTER(AegisPlanMatmul), u64, u64p]),
+    ("aegis_plan_note", ctypes.c_char_p, [vp]),
+    ("aegis_plan_free", ctypes.c_int, [vp]),
+    ("aegis_graph_comm_bytes", ctypes.c_int, [vp, u64p]),
     ("aegis_graph_owned_lanes", ctypes.c_int, [vp, u32, ctypes.POINTER(ctypes.c_uint8), u32]),
     ("aegis_graph_shard_info", ctypes.c_int, [vp, u32p, u32p, u32p, u32p, u32p]),
     ("aegis_graph_set_hoisting", ctypes.c_int, [vp, ctypes.c_int]),
@@ -133,9 +168,15 @@ SIGNATURES = [
     ("aegis_graph_peak_bytes", u64, [vp]),
     ("aegis_p2p_create", ctypes.c_int, [vp, u64, vp, ctypes.POINTER(vp)]),
     ("aegis_p2p_open", ctypes.c_int, [vp, vp, vp, u32, u32]),
+    ("aegis_p2p_open_local", ctypes.c_int, [vp, vp, ctypes.POINTER(vp), u32, u32]),
     ("aegis_p2p_stage", ctypes.c_int, [vp, vp, vp, u64]),
     ("aegis_p2p_reduce", ctypes.c_int, [vp, vp, vp, u64, u32]),
     ("aegis_p2p_destroy", ctypes.c_int, [vp]),
+    ("aegis_graph_p2p_bytes", ctypes.c_int, [vp, u64p]),
+    ("aegis_graph_set_p2p", ctypes.c_int, [vp, vp]),
+    ("aegis_graph_set_fault", ctypes.c_int, [vp, ctypes.c_int]),
+    ("aegis_graph_set_stored_weights", ctypes.c_int, [vp, ctypes.c_int]),
+    ("aegis_pmult_acc_stored", ctypes.c_int, [vp, vp, u32, u32, u32, vp, u32, u32, vp, u32, u32, u32]),
 ]
 
 # int (*)(void* user, uint64_t* buf, uint64_t words_per_rank, uint32_t group)

@@ -150,11 +150,36 @@ class Context:
         self._call("aegis_probe_read", ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b))
         return n.value, ms.value, b.value
 
+    # -- peer-memory windows (csrc/p2p.cu) --
+    def p2p_window(self, nbytes):
+        """A window of `nbytes` data bytes; returns a P2pWindow (with .handle, its 64-byte IPC handle)."""
+        raw = (ctypes.c_char * 64)()
+        h = ctypes.c_void_p()
+        self._call("aegis_p2p_create", nbytes, ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(h))
+        return P2pWindow(self, h, bytes(raw), nbytes)
+
     # -- bundles / keys --
     def bundle(self, lanes, comps, level):
         h = ctypes.c_void_p()
         self._call("aegis_bundle_alloc", lanes, comps, level, ctypes.byref(h))
         return Bundle(self, h, lanes, comps, level)
+
+    def bundle_load(self, path):
+        """A bundle from an aegis store file (csrc/store.cu), streamed to the device and hash-checked."""
+        h = ctypes.c_void_p()
+        self._call("aegis_bundle_load", str(path).encode(), ctypes.byref(h))
+        lanes, comps, level = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        self.lib.aegis_bundle_info(h, ctypes.byref(lanes), ctypes.byref(comps), ctypes.byref(level), None)
+        return Bundle(self, h, lanes.value, comps.value, level.value)
+
+    def bundle_save(self, b, path):
+        self._call("aegis_bundle_save", b.h, str(path).encode())
+
+    def keys_save(self, key_id, path):
+        self._call("aegis_keys_save", key_id, str(path).encode())
+
+    def keys_load(self, key_id, path):
+        self._call("aegis_keys_load", key_id, str(path).encode())
 
     def keys_generate(self, ids):
         a = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
@@ -259,6 +284,10 @@ class Context:
     def pmult_acc(self, acc, x, weight_bundle, weight_lanes, level, chunk_period=0):
         self._call("aegis_pmult_acc", acc.h, 0, acc.lanes, chunk_period, x.h, 0, x.lanes,
                    weight_bundle, weight_lanes, level)
+
+    def pmult_acc_stored(self, acc, x, w, level, chunk_period=0, w_slice=None):
+        wl, wc = w_slice or (0, w.lanes)
+        self._call("aegis_pmult_acc_stored", acc.h, 0, acc.lanes, chunk_period, x.h, 0, x.lanes, w.h, wl, wc, level)
 
     # -- graphs --
     def graph(self, kind=0, tokens=128, layers=1, model_dim=768, ffn_dim=3072, head_dim=64,
@@ -381,6 +410,44 @@ class Graph:
         self._reducer = L.REDUCE_FN(cb)  # keep alive
         self.lib.aegis_graph_set_reducer(self.h, ctypes.cast(self._reducer, ctypes.c_void_p), None)
 
+    def plan(self, world, reorder=True):
+        """The Aegis execution plan on `world` devices (aegis_plan_build): a Plan."""
+        h = ctypes.c_void_p()
+        rc = self.lib.aegis_plan_build(self.h, world, 1 if reorder else 0, ctypes.byref(h))
+        if rc:
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+        return Plan(self.lib, h)
+
+    def comm_bytes(self):
+        """Bytes this rank sent through PCMM exchanges in the last run."""
+        v = ctypes.c_uint64()
+        self.lib.aegis_graph_comm_bytes(self.h, ctypes.byref(v))
+        return v.value
+
+    def p2p_bytes(self):
+        """Window bytes the device-synchronised PCMM exchange needs under the current shard (0: none)."""
+        v = ctypes.c_uint64()
+        rc = self.lib.aegis_graph_p2p_bytes(self.h, ctypes.byref(v))
+        if rc:
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+        return v.value
+
+    def set_p2p(self, window):
+        """Attach a p2p window (Context.p2p_window): sharded PCMM sums are exchanged on the comm
+        stream with device-side flags; no reduce hook needed (None detaches)."""
+        self._p2p = window  # keep alive while attached
+        self.lib.aegis_graph_set_p2p(self.h, window.h if window is not None else None)
+
+    def set_stored_weights(self, enable):
+        """Stored-plaintext PCMM (weights written to HBM by the Encode ops, read by PMult)."""
+        self.lib.aegis_graph_set_stored_weights(self.h, 1 if enable else 0)
+
+    def set_fault(self, kind):
+        """Fault injection (tests): 1 drops the PCMM exchange, 0 restores it."""
+        rc = self.lib.aegis_graph_set_fault(self.h, kind)
+        if rc:
+            raise ValueError("bad fault kind")
+
     def set_hoisting(self, enable):
         self.lib.aegis_graph_set_hoisting(self.h, 1 if enable else 0)
 
@@ -448,3 +515,65 @@ class Graph:
             self.free()
         except Exception:
             pass
+
+
+class P2pWindow:
+    """A rank's peer-memory window (aegis_p2p_*); open it over its group with
+    open_ipc (separate processes) or open_local (contexts of one process)."""
+
+    def __init__(self, ctx, h, handle, nbytes):
+        self.ctx, self.h, self.handle, self.nbytes = ctx, h, handle, nbytes
+
+    def open_ipc(self, handles, self_rank):
+        allh = ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
+        self.ctx._call("aegis_p2p_open", self.h, ctypes.cast(allh, ctypes.c_void_p), len(handles), self_rank)
+
+    def open_local(self, windows, self_rank):
+        arr = (ctypes.c_void_p * len(windows))(*[w.h for w in windows])
+        self.ctx._call("aegis_p2p_open_local", self.h, arr, len(windows), self_rank)
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.aegis_p2p_destroy(self.h)
+            self.h = None
+
+
+class Plan:
+    """aegis_plan_* wrapper: summary(), events(), device(d), matmuls(), note."""
+    CATEGORIES = ("ffn", "attention", "layernorm", "boot", "other")
+    MODES = ("local", "gather_inputs", "reduce_outputs")
+
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.aegis_plan_free(self.h)
+        except Exception:
+            pass
+
+    def summary(self):
+        s = L.AegisPlanSummary()
+        self.lib.aegis_plan_summary_get(self.h, ctypes.byref(s))
+        return {f: getattr(s, f) for f, _ in s._fields_ if f != "pad"}
+
+    def _list(self, fn, typ, *pre):
+        n = ctypes.c_uint64()
+        getattr(self.lib, fn)(self.h, *pre, None, 0, ctypes.byref(n))
+        arr = (typ * max(1, n.value))()
+        getattr(self.lib, fn)(self.h, *pre, arr, n.value, ctypes.byref(n))
+        return [{f: getattr(a, f) for f, _ in a._fields_} for a in list(arr)[:n.value]]
+
+    def events(self):
+        return self._list("aegis_plan_events", L.AegisPlanEvent)
+
+    def device(self, d):
+        return self._list("aegis_plan_device", L.AegisPlanInstr, d)
+
+    def matmuls(self):
+        return self._list("aegis_plan_matmuls", L.AegisPlanMatmul)
+
+    @property
+    def note(self):
+        return (self.lib.aegis_plan_note(self.h) or b"").decode()

@@ -12,7 +12,9 @@
 #include "context.h"
 #include "executor.h"
 #include "p2p.h"
+#include "plan.h"
 #include "heplan_ir.h"
+#include "store.h"
 
 using aegis::Bundle;
 using aegis::Context;
@@ -28,6 +30,9 @@ struct aegis_ctx {
 };
 struct aegis_bundle {
   Bundle* b = nullptr;
+};
+struct aegis_p2p {
+  std::unique_ptr<aegis::P2pWindow> w;
 };
 
 namespace {
@@ -87,11 +92,14 @@ struct aegis_graph {
   std::unique_ptr<aegis::ShardPlan> shard;
   std::unique_ptr<aegis::ShardPlan> hash_lanes;  // aegis_graph_set_hash_group
   aegis::ReduceFn reduce = nullptr;
+  aegis::P2pWindow* p2p = nullptr;  // device-synchronised exchange window (not owned)
+  int fault = 0;
+  int stored_weights = 0;
   void* reduce_user = nullptr;
   int hoist = 1;
   int dce = 0;
   int wrap_defer = 1;
-  uint64_t h2d = 0, d2h = 0;
+  uint64_t h2d = 0, d2h = 0, comm = 0;
   bool profile = false;
   std::vector<float> op_ms;
 };
@@ -115,6 +123,9 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.hash_lanes = g->hash_lanes.get();
   opt.reduce = g->reduce;
   opt.reduce_user = g->reduce_user;
+  opt.p2p = g->shard && g->shard->m > 1 ? g->p2p : nullptr;
+  opt.fault = g->fault;
+  opt.stored_weights = g->stored_weights != 0;
   opt.hoist = g->hoist != 0;
   opt.dce = g->dce != 0;
   opt.wrap_defer = g->wrap_defer != 0;
@@ -125,6 +136,7 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   aegis::Executor ex(c, g->g, opt);
   ex.run();
   g->h2d = ex.h2d_bytes;
+  g->comm = ex.comm_bytes;
   g->d2h = ex.d2h_bytes;
   g->peak = c.peak_bytes;
 }
@@ -276,6 +288,37 @@ int aegis_keys_upload(aegis_ctx* ctx, uint64_t key_id, const uint64_t* host, uin
   return guard(ctx, [&] {
     if (!host) throw Error(AEGIS_EINVAL, "key upload: null host buffer");
     ctx->c->upload_key(key_id, reinterpret_cast<const aegis::u64*>(host), words, coeff_domain != 0);
+  });
+}
+int aegis_bundle_save(aegis_ctx* ctx, const aegis_bundle* b, const char* path) {
+  return guard(ctx, [&] {
+    if (!path) throw Error(AEGIS_EINVAL, "null path");
+    aegis::store_save_bundle(*ctx->c, need(b), path);
+  });
+}
+int aegis_bundle_load(aegis_ctx* ctx, const char* path, aegis_bundle** out) {
+  return guard(ctx, [&] {
+    if (!path || !out) throw Error(AEGIS_EINVAL, "null argument");
+    auto* h = new aegis_bundle;
+    try {
+      h->b = aegis::store_load_bundle(*ctx->c, path);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+int aegis_keys_save(aegis_ctx* ctx, uint64_t key_id, const char* path) {
+  return guard(ctx, [&] {
+    if (!path) throw Error(AEGIS_EINVAL, "null path");
+    aegis::store_save_key(*ctx->c, key_id, path);
+  });
+}
+int aegis_keys_load(aegis_ctx* ctx, uint64_t key_id, const char* path) {
+  return guard(ctx, [&] {
+    if (!path) throw Error(AEGIS_EINVAL, "null path");
+    aegis::store_load_key(*ctx->c, key_id, path);
   });
 }
 int aegis_keys_bytes(const aegis_ctx* ctx, uint64_t* out) {
@@ -835,6 +878,136 @@ int aegis_graph_set_reducer(aegis_graph* g, aegis_reduce_fn fn, void* user) {
   g->reduce_user = user;
   return AEGIS_OK;
 }
+struct aegis_plan {
+  aegis::ExecPlan p;
+};
+int aegis_plan_build(const aegis_graph* g, uint32_t world, int reorder, aegis_plan** out) {
+  return guard(nullptr, [&] {
+    if (!g || !out || world == 0) throw Error(AEGIS_EINVAL, "plan_build: bad argument");
+    auto pl = std::make_unique<aegis_plan>();
+    pl->p = aegis::build_plan(g->g, token_groups(g), world, (uint32_t)header_value(g->header, "N"), reorder != 0);
+    *out = pl.release();
+  });
+}
+int aegis_plan_summary_get(const aegis_plan* p, aegis_plan_summary* out) {
+  if (!p || !out) return AEGIS_EINVAL;
+  const aegis::ExecPlan& P = p->p;
+  aegis_plan_summary s{};
+  s.world = P.world;
+  s.token_groups = P.tg_total;
+  s.ranks_per_group = P.m;
+  s.reordered = P.reordered;
+  s.executable = P.executable;
+  s.matmuls = (uint32_t)P.matmuls.size();
+  s.events = P.events.size();
+  for (const auto& d : P.devices) s.instrs_total += d.compute.size();
+  for (const auto& e : P.events) {
+    s.events_executed += e.executed;
+    s.bytes_total += e.bytes_total;
+    uint64_t* cat[] = {&s.bytes_ffn, &s.bytes_attention, &s.bytes_layernorm, &s.bytes_boot, &s.bytes_other};
+    *cat[(int)e.category] += e.bytes_total;
+  }
+  for (const auto& m : P.matmuls) {
+    s.matmuls_gather_chosen += m.chosen == aegis::MatmulMode::kGatherInputs;
+    s.bytes_reference_rule += m.chosen == aegis::MatmulMode::kGatherInputs ? m.gather_bytes
+                              : m.chosen == aegis::MatmulMode::kReduceOutputs ? m.reduce_bytes : 0;
+  }
+  *out = s;
+  return AEGIS_OK;
+}
+int aegis_plan_events(const aegis_plan* p, aegis_plan_event* out, uint64_t cap, uint64_t* n) {
+  if (!p || !n) return AEGIS_EINVAL;
+  *n = p->p.events.size();
+  if (out)
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, *n); ++i) {
+      const aegis::PlanEvent& e = p->p.events[i];
+      out[i] = aegis_plan_event{e.id, (uint32_t)e.kind, (uint32_t)e.semantic, e.dev_lo, e.dev_count, e.bundle, e.lane,
+                                e.lane_count, e.level, (uint32_t)e.category, e.app_node, e.he_op, e.executed,
+                                e.bytes_per_device, e.bytes_total};
+    }
+  return AEGIS_OK;
+}
+int aegis_plan_device(const aegis_plan* p, uint32_t device, aegis_plan_instr* out, uint64_t cap, uint64_t* n) {
+  if (!p || !n || device >= p->p.devices.size()) return AEGIS_EINVAL;
+  const auto& C = p->p.devices[device].compute;
+  *n = C.size();
+  if (out)
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, *n); ++i)
+      out[i] = aegis_plan_instr{C[i].op, C[i].lane, C[i].lane_count, C[i].flags, C[i].wait_event};
+  return AEGIS_OK;
+}
+int aegis_plan_matmuls(const aegis_plan* p, aegis_plan_matmul* out, uint64_t cap, uint64_t* n) {
+  if (!p || !n) return AEGIS_EINVAL;
+  *n = p->p.matmuls.size();
+  if (out)
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, *n); ++i) {
+      const aegis::MatmulInfo& m = p->p.matmuls[i];
+      out[i] = aegis_plan_matmul{m.app_node, m.acc_bundle, m.input_bundle, m.ship_bundle, (uint32_t)m.chosen,
+                                 (uint32_t)m.executed, m.gather_bytes, m.reduce_bytes};
+    }
+  return AEGIS_OK;
+}
+const char* aegis_plan_note(const aegis_plan* p) { return p ? p->p.note.c_str() : ""; }
+int aegis_plan_free(aegis_plan* p) {
+  delete p;
+  return AEGIS_OK;
+}
+int aegis_graph_comm_bytes(const aegis_graph* g, uint64_t* bytes) {
+  if (!g || !bytes) return AEGIS_EINVAL;
+  *bytes = g->comm;
+  return AEGIS_OK;
+}
+int aegis_graph_p2p_bytes(const aegis_graph* g, uint64_t* bytes) {
+  if (!g || !bytes) return AEGIS_EINVAL;
+  return guard(nullptr, [&] {
+    uint64_t best = 0;
+    const uint32_t m = g->shard ? g->shard->m : 1;
+    if (m > 1) {
+      const uint64_t n = header_value(g->header, "N");
+      for (const hp::HeOp& op : g->g.ops) {
+        if (op.kind != hp::HeOpKind::kPMult || op.ins.size() != 2) continue;
+        const hp::CtBundle& acc = g->g.bundles[op.out.bundle];
+        const aegis::PcmmShape sh = aegis::pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count,
+                                                      acc.chunk_period);
+        const uint64_t share = sh.c_sub / m;
+        best = std::max<uint64_t>(best, share * std::max<uint32_t>(2, acc.components) * acc.level * n);
+      }
+    }
+    *bytes = 2 * (uint64_t)m * best * 8;  // two parities x m slots x the largest share
+  });
+}
+int aegis_graph_set_p2p(aegis_graph* g, aegis_p2p* w) {
+  if (!g) return AEGIS_EINVAL;
+  g->p2p = w ? w->w.get() : nullptr;
+  return AEGIS_OK;
+}
+int aegis_graph_set_stored_weights(aegis_graph* g, int enable) {
+  if (!g) return AEGIS_EINVAL;
+  g->stored_weights = enable != 0;
+  return AEGIS_OK;
+}
+int aegis_pmult_acc_stored(aegis_ctx* ctx, aegis_bundle* acc, uint32_t acc_lane, uint32_t acc_lanes,
+                           uint32_t chunk_period, const aegis_bundle* x, uint32_t x_lane, uint32_t x_lanes,
+                           const aegis_bundle* w, uint32_t w_lane, uint32_t w_lanes, uint32_t level) {
+  return guard(ctx, [&] {
+    Bundle& A = need(acc);
+    const Bundle& X = need(x);
+    const Bundle& W = need(w);
+    check_lanes(A, acc_lane, acc_lanes, "pmult");
+    check_lanes(X, x_lane, x_lanes, "pmult");
+    check_lanes(W, w_lane, w_lanes, "pmult");
+    check_level(A, level, "pmult");
+    check_level(X, level, "pmult");
+    check_level(W, level, "pmult");
+    ctx->c->op_pmult(A, acc_lane, acc_lanes, chunk_period, X, x_lane, x_lanes, 0, w_lanes, level, 0, ~0u, 0, ~0u, &W,
+                     w_lane);
+  });
+}
+int aegis_graph_set_fault(aegis_graph* g, int kind) {
+  if (!g || kind < 0 || kind > 1) return AEGIS_EINVAL;
+  g->fault = kind;
+  return AEGIS_OK;
+}
 int aegis_graph_owned_lanes(const aegis_graph* g, uint32_t bundle, uint8_t* mask, uint32_t cap) {
   if (!g || bundle >= g->g.bundles.size()) return AEGIS_EINVAL;
   const uint32_t lanes = g->g.bundles[bundle].lanes;
@@ -989,10 +1162,6 @@ int aegis_graph_free(aegis_graph* g) {
 uint64_t aegis_graph_peak_bytes(const aegis_graph* g) { return g ? g->peak : 0; }
 
 
-struct aegis_p2p {
-  std::unique_ptr<aegis::P2pWindow> w;
-};
-
 int aegis_p2p_create(aegis_ctx* ctx, uint64_t bytes, void* handle_out, aegis_p2p** out) {
   if (!ctx || !handle_out || !out) return AEGIS_EINVAL;
   return guard(ctx, [&] {
@@ -1009,6 +1178,14 @@ int aegis_p2p_create(aegis_ctx* ctx, uint64_t bytes, void* handle_out, aegis_p2p
 int aegis_p2p_open(aegis_ctx* ctx, aegis_p2p* w, const void* handles, uint32_t m, uint32_t self) {
   if (!ctx || !w || !handles) return AEGIS_EINVAL;
   return guard(ctx, [&] { aegis::p2p_open(*w->w, handles, m, self); });
+}
+int aegis_p2p_open_local(aegis_ctx* ctx, aegis_p2p* w, aegis_p2p* const* group, uint32_t m, uint32_t self) {
+  if (!ctx || !w || !group) return AEGIS_EINVAL;
+  return guard(ctx, [&] {
+    std::vector<aegis::P2pWindow*> v;
+    for (uint32_t r = 0; r < m; ++r) v.push_back(group[r] ? group[r]->w.get() : nullptr);
+    aegis::p2p_open_local(*w->w, v, self);
+  });
 }
 int aegis_p2p_stage(aegis_ctx* ctx, aegis_p2p* w, const uint64_t* buf, uint64_t words) {
   if (!ctx || !w || !buf) return AEGIS_EINVAL;

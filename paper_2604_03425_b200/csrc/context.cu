@@ -437,6 +437,30 @@ u64 Context::galois_of(int offset) const {  // 5^offset mod 2N (rns_math.hpp:142
   for (long long i = 0; i < ofs; ++i) gk = (gk * 5) % order;
   return gk;
 }
+u64* Context::key_storage(u64 key_id, bool create) {
+  auto it = keys_.find(key_id);
+  if (it != keys_.end()) return it->second;
+  if (!create) return nullptr;
+  u64* k = alloc_key();
+  keys_[key_id] = k;
+  return k;
+}
+
+void Context::drop_key(u64 key_id) {
+  auto it = keys_.find(key_id);
+  if (it == keys_.end()) return;
+  cudaStreamSynchronize(stream);
+  cudaFree(it->second);
+  keys_.erase(it);
+}
+
+u64 Context::chain_fingerprint() const {
+  u64 h = mix64(log_n * kGold + chain);
+  for (u32 i = 0; i < chain; ++i) h = mix64(h ^ (primes_[i] + (i + 1) * kGold));
+  for (u32 i = 0; i < kAlpha; ++i) h = mix64(h ^ (primes_[kSpecialBase + i] + (i + 101) * kGold));
+  return h;
+}
+
 const u64* Context::key(u64 key_id) {
   auto it = keys_.find(key_id);
   if (it == keys_.end()) generate_key(key_id);
@@ -912,14 +936,19 @@ void Context::op_cadd(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, Lan
 
 void Context::op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
                        u32 x_lanes, u32 wbundle, u32 wlanes, u32 level, u32 t_lo, u32 t_hi, u32 ci_lo,
-                       u32 ci_hi) {
+                       u32 ci_hi, const Bundle* wst, u32 w_lane0) {
   const PcmmShape sh = pcmm_shape(x_lanes, acc_lanes, wlanes, chunk_period);
   t_hi = std::min(t_hi, sh.tg);
   ci_hi = std::min(ci_hi, sh.c_in);
   if (t_lo >= t_hi || ci_lo >= ci_hi) return;
-  u64* rk = alloc((size_t)wlanes * level);
-  AEGIS_CHECK_CUDA(launch_weight_rowkeys(rk, wlanes, level, seed_weight, wbundle, stream));
-  count();
+  if (wst && (wst->comps != 1 || wst->level < level || (uint64_t)w_lane0 + wlanes > wst->lanes))
+    throw Error(AEGIS_EINVAL, "stored PMult weights: need a 1-component bundle covering the weight lanes and level");
+  u64* rk = nullptr;
+  if (!wst) {
+    rk = alloc((size_t)wlanes * level);
+    AEGIS_CHECK_CUDA(launch_weight_rowkeys(rk, wlanes, level, seed_weight, wbundle, stream));
+    count();
+  }
   for (u32 s = 0; s < sh.S; ++s) {
     // sub-tensor s occupies acc lanes [s*chunk, (s+1)*chunk), token-major inside
     PmultArgs a;
@@ -938,6 +967,10 @@ void Context::op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_perio
     a.limbs = level;
     a.n = n;
     a.rowkeys = rk;
+    if (wst) {
+      a.wst = wst->view();
+      a.w_lane0 = w_lane0;
+    }
     AEGIS_CHECK_CUDA(launch_pmult_acc(a, d_pc, stream));
     count((a.tg + 3) / 4);
   }

@@ -79,6 +79,13 @@ class Context {
   void generate_key(u64 key_id);
   void upload_key(u64 key_id, const u64* host, size_t words, bool coeff_domain);
   const u64* key(u64 key_id);
+  // device storage of key `key_id` in the internal (pre-permuted) layout:
+  // the existing key, or a fresh uninitialised one (store.cu loads into it)
+  u64* key_storage(u64 key_id, bool create);
+  void drop_key(u64 key_id);
+  // fingerprint of the prime chain (main + special): files written under a
+  // different chain are rejected (store.cu)
+  u64 chain_fingerprint() const;
   u32 key_slots() const { return chain + kAlpha; }
   u32 key_digits() const { return (chain + kAlpha - 1) / kAlpha; }
   size_t key_bytes() const { return (size_t)key_digits() * 2 * key_slots() * n * 8; }
@@ -152,7 +159,7 @@ class Context {
   // step (defaults: everything); a position subset yields partial sums.
   void op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
                 u32 x_lanes, u32 wbundle, u32 wlanes, u32 level, u32 t_lo = 0, u32 t_hi = ~0u, u32 ci_lo = 0,
-                u32 ci_hi = ~0u);
+                u32 ci_hi = ~0u, const Bundle* wstored = nullptr, u32 w_lane0 = 0);
 
   void count(u64 k = 1) { launches += k; }
   // workspace budget of one operator phase: `gib` GiB scaled by AEGIS_WS_SCALE

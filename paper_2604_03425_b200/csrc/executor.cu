@@ -28,9 +28,12 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
   zero_first.assign(nb, 0);
   partial.assign(nb, 0);
   donated.assign(nb, 0);
+  is_weight.assign(nb, 0);
   shadow.assign(nb, nullptr);
   shadow_level.assign(nb, 0);
   last_use.assign(nb, -1);
+  last_pmult.assign(nb, -1);
+  pending.assign(nb, {});
   std::vector<char> seen(nb, 0);
   for (size_t i = 0; i < nb; ++i) alloc_comps[i] = g.bundles[i].components;
   for (size_t i = 0; i < g.ops.size(); ++i) {
@@ -38,6 +41,8 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
     last_use[op.out.bundle] = (int64_t)i;
     for (auto& s : op.ins) last_use[s.bundle] = (int64_t)i;
     if (op.kind == hp::HeOpKind::kCMult) alloc_comps[op.out.bundle] = 3;
+    if (op.kind == hp::HeOpKind::kPMult) last_pmult[op.out.bundle] = (int64_t)i;
+    if (op.kind == hp::HeOpKind::kEncode) is_weight[op.out.bundle] = 1;
     if (!seen[op.out.bundle] && op.kind != hp::HeOpKind::kEncode) {
       seen[op.out.bundle] = 1;
       zero_first[op.out.bundle] = op.accumulate ? 1 : 0;
@@ -90,6 +95,11 @@ void Executor::find_live_lanes() {
 }
 
 Executor::~Executor() {
+  if (!events.empty()) {  // the comm stream may still read bundles freed below
+    cudaStreamSynchronize(c.comm);
+    cudaStreamSynchronize(c.stream);
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+  }
   for (auto& gr : groups)
     if (gr.ext) c.release(gr.ext);
   for (Bundle* S : shadow) c.free_bundle(S);
@@ -98,23 +108,39 @@ Executor::~Executor() {
 }
 
 Bundle& Executor::get(u32 id) {
+  if (!pending[id].empty()) wait_pending(id);
   if (!buf[id]) {
     const hp::CtBundle& cb = g.bundles[id];
-    buf[id] = c.new_bundle(cb.lanes, std::max<u32>(2, alloc_comps[id]), cb.level, zero_first[id] != 0);
+    const u32 comps = is_weight[id] ? 1 : std::max<u32>(2, alloc_comps[id]);
+    buf[id] = c.new_bundle(cb.lanes, comps, cb.level, zero_first[id] != 0);
     cur_comps[id] = 2;
   }
   return *buf[id];
 }
 
-Bundle& Executor::input(const hp::LaneSlice& s) {
+Bundle& Executor::input(const hp::LaneSlice& s, u32 lo, u32 hi) {
   if (shadow[s.bundle]) materialize(s.bundle);
   if (!buf[s.bundle]) throw Error(AEGIS_ELOGIC, "op reads bundle " + g.bundles[s.bundle].tag + " before it is written");
   if (partial[s.bundle]) reduce_partial(s.bundle);
+  if (!pending[s.bundle].empty()) wait_pending(s.bundle, lo, hi);
   return *buf[s.bundle];
+}
+
+void Executor::wait_pending(u32 b, u32 lo, u32 hi) {
+  std::vector<Pending>& v = pending[b];
+  for (size_t k = 0; k < v.size();) {
+    if (v[k].lo < hi && lo < v[k].hi) {
+      AEGIS_CHECK_CUDA(cudaStreamWaitEvent(c.stream, v[k].ev, 0));
+      v.erase(v.begin() + (long)k);
+    } else {
+      ++k;
+    }
+  }
 }
 
 void Executor::retire(u32 id) {
   if (shadow[id]) materialize(id);
+  if (!pending[id].empty()) wait_pending(id);
   if (!buf[id]) return;
   if (donated[id]) {  // storage now belongs to the op's output bundle
     buf[id] = nullptr;
@@ -135,7 +161,7 @@ void Executor::retire(u32 id) {
       d2h_bytes += (size_t)(e - s) * lane_words * 8;
     }
   }
-  if (o.d_hash) hash_bundle(id, b);
+  if (o.d_hash && !is_weight[id]) hash_bundle(id, b);
   c.free_bundle(buf[id]);
   buf[id] = nullptr;
 }
@@ -143,6 +169,7 @@ void Executor::retire(u32 id) {
 // DESIGN.md §2.4 content hash of the lanes this rank owns (or, with
 // hash_lanes, of that plan's lanes only) into o.d_hash[id]
 void Executor::hash_bundle(u32 id, const Bundle& b) {
+  if (!pending[id].empty()) wait_pending(id);
   const u32 lanes = g.bundles[id].lanes;
   const ShardPlan* hp_ = o.hash_lanes ? o.hash_lanes : o.shard;
   std::vector<std::pair<u32, u32>> runs =
@@ -304,21 +331,23 @@ LaneMap Executor::sub_map(const hp::LaneSlice& s, u32 n, u32 pos, u32 len) {
   return s.lane_count == n ? LaneMap{s.lane + pos, len} : LaneMap{s.lane + pos % s.lane_count, len};
 }
 
-void Executor::pmult(const hp::HeOp& op) {
+void Executor::pmult(const hp::HeOp& op, int64_t i) {
   if (!op.accumulate || op.ins.size() != 2) throw Error(AEGIS_ELOGIC, "unsupported PMult form");
   Bundle& x = input(op.ins[0]);
   Bundle& acc = get(op.out.bundle);
   const u32 chunk = g.bundles[op.out.bundle].chunk_period;
   const u32 L = op.use_level;
+  const Bundle* ws = o.stored_weights ? &input(op.ins[1]) : nullptr;
+  const u32 wl0 = op.ins[1].lane;
   if (!o.shard) {
     c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
-               op.ins[1].lane_count, L);
+               op.ins[1].lane_count, L, 0, ~0u, 0, ~0u, ws, wl0);
     return;
   }
   const ShardPlan& P = *o.shard;
   if (P.m == 1) {
     c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
-               op.ins[1].lane_count, L, P.tg_lo, P.tg_hi);
+               op.ins[1].lane_count, L, P.tg_lo, P.tg_hi, 0, ~0u, ws, wl0);
     return;
   }
   // input-stationary: this rank's input positions into every output of its group
@@ -332,8 +361,48 @@ void Executor::pmult(const hp::HeOp& op) {
     }
   if (ci_lo < ci_hi)
     c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
-               op.ins[1].lane_count, L, t, t + 1, ci_lo, ci_hi);
+               op.ins[1].lane_count, L, t, t + 1, ci_lo, ci_hi, ws, wl0);
   partial[op.out.bundle] = 1;
+  // the accumulator is complete on this rank: start its exchange now, on the comm stream
+  if (o.p2p && last_pmult[op.out.bundle] == i) reduce_async(op.out.bundle);
+}
+
+// Device-synchronised form of reduce_partial: one p2p_exchange per sub-tensor
+// on the comm stream, started right after the last PMult of the accumulator;
+// the compute stream waits (cudaStreamWaitEvent) only when an op touches the
+// sub-tensor's lanes, so the rescale of sub-tensor s overlaps the exchange of
+// sub-tensor s + 1.
+void Executor::reduce_async(u32 b) {
+  partial[b] = 0;
+  const ShardPlan& P = *o.shard;
+  Bundle& acc = *buf[b];
+  const hp::HeOp& pm = g.ops[last_pmult[b]];
+  const PcmmShape sh = pcmm_shape(pm.ins[0].lane_count, pm.out.lane_count, pm.ins[1].lane_count,
+                                  g.bundles[b].chunk_period);
+  if (sh.c_sub % P.m) throw Error(AEGIS_EINVAL, "PCMM outputs do not split evenly over the ranks of a token group");
+  const u32 t = P.tg_lo, share = sh.c_sub / P.m;
+  const uint64_t words_per_lane = (uint64_t)acc.comps * acc.level * c.n;
+  cudaEvent_t ready;
+  AEGIS_CHECK_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  events.push_back(ready);
+  AEGIS_CHECK_CUDA(cudaEventRecord(ready, c.stream));
+  AEGIS_CHECK_CUDA(cudaStreamWaitEvent(c.comm, ready, 0));
+  for (u32 s = 0; s < sh.S; ++s) {
+    const u32 lane0 = pm.out.lane + pcmm_lane(sh, t, s * sh.c_sub);
+    if (o.fault != 1) {
+      p2p_exchange(*o.p2p, acc.view().limb(lane0, 0, 0, c.n), words_per_lane * share, c.comm);
+      c.count(4);
+      comm_bytes += (size_t)(P.m - 1) * words_per_lane * share * 8;
+    }
+    const u32 mine = lane0 + P.part * share;
+    AEGIS_CHECK_CUDA(launch_reduce_lanes(acc.view(), mine, share, acc.comps, acc.level, c.n, c.d_pc, c.comm));
+    c.count();
+    cudaEvent_t done;
+    AEGIS_CHECK_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    events.push_back(done);
+    AEGIS_CHECK_CUDA(cudaEventRecord(done, c.comm));
+    pending[b].push_back(Pending{mine, mine + share, done});
+  }
 }
 
 // Sum the partial accumulators of this rank's token group over its m ranks
@@ -341,7 +410,8 @@ void Executor::pmult(const hp::HeOp& op) {
 void Executor::reduce_partial(u32 b) {
   partial[b] = 0;
   if (!o.shard || o.shard->m == 1) return;
-  if (!o.reduce) throw Error(AEGIS_ELOGIC, "sharded PCMM needs a reduce-scatter hook (aegis_graph_set_reducer)");
+  if (!o.reduce && o.fault != 1)
+    throw Error(AEGIS_ELOGIC, "sharded PCMM needs a reduce-scatter hook (aegis_graph_set_reducer) or a p2p window");
   const ShardPlan& P = *o.shard;
   Bundle& acc = *buf[b];
   // find the PCMM shape from the last PMult writing this bundle
@@ -358,8 +428,11 @@ void Executor::reduce_partial(u32 b) {
   for (u32 s = 0; s < sh.S; ++s) {
     const u32 lane0 = pm->out.lane + pcmm_lane(sh, t, s * sh.c_sub);
     u64* base = acc.view().limb(lane0, 0, 0, c.n);
-    if (o.reduce(o.reduce_user, base, words_per_lane * share, t) != 0)
-      throw Error(AEGIS_ENCCL, "reduce-scatter hook failed");
+    if (o.fault != 1) {
+      if (o.reduce(o.reduce_user, base, words_per_lane * share, t) != 0)
+        throw Error(AEGIS_ENCCL, "reduce-scatter hook failed");
+      comm_bytes += (size_t)(P.m - 1) * words_per_lane * share * 8;
+    }
     AEGIS_CHECK_CUDA(launch_reduce_lanes(acc.view(), lane0 + P.part * share, share, acc.comps, acc.level, c.n, c.d_pc,
                                          c.stream));
     c.count();
@@ -400,7 +473,7 @@ void Executor::donate(const hp::HeOp& op, int64_t i) {
 // to the op-by-op order; the 64 full-width read-modify-writes (~160 GB each
 // way in total per op) become 64 narrow ones plus one wide one.
 bool Executor::wrap_deferrable(const hp::HeOp& op) const {
-  if (!o.wrap_defer || o.shard || o.dce || op.kind != hp::HeOpKind::kCAdd || !op.accumulate || op.ins.size() != 1)
+  if (!o.wrap_defer || o.dce || op.kind != hp::HeOpKind::kCAdd || !op.accumulate || op.ins.size() != 1)
     return false;
   const hp::LaneSlice& s = op.ins[0];
   const u32 n = g.bundles[op.out.bundle].lanes, m = s.lane_count;
@@ -413,7 +486,17 @@ void Executor::materialize(u32 b) {
   Bundle* S = shadow[b];
   shadow[b] = nullptr;
   Bundle& X = get(b);
-  c.op_cadd(X, 0, g.bundles[b].lanes, *S, LaneMap{0, S->lanes}, nullptr, LaneMap{0, 1}, shadow_level[b], true);
+  const u32 lanes = g.bundles[b].lanes, m = S->lanes;
+  if (!o.shard) {
+    c.op_cadd(X, 0, lanes, *S, LaneMap{0, m}, nullptr, LaneMap{0, 1}, shadow_level[b], true);
+  } else {  // owned lanes only, split where the operand index j mod m wraps
+    for (auto [rs, re] : o.shard->runs(b, 0, lanes))
+      for (u32 pos = rs; pos < re;) {
+        const u32 end = std::min(re, (pos / m + 1) * m);
+        c.op_cadd(X, pos, end - pos, *S, LaneMap{pos % m, end - pos}, nullptr, LaneMap{0, 1}, shadow_level[b], true);
+        pos = end;
+      }
+  }
   c.free_bundle(S);
   cur_comps[b] = 2;
 }
@@ -421,7 +504,15 @@ void Executor::materialize(u32 b) {
 void Executor::step(const hp::HeOp& op, int64_t i) {
   using K = hp::HeOpKind;
   const u32 L = op.use_level;
-  if (op.kind == K::kEncode) return;  // weights are generated inside the PMult kernel (kGenerate)
+  if (op.kind == K::kEncode) {
+    if (!o.stored_weights) return;  // weights are generated inside the PMult kernel (kGenerate)
+    Bundle& w = get(op.out.bundle);  // stored form: the kGenerate rows land in HBM
+    AEGIS_CHECK_CUDA(launch_limb_generate(w.view(), 0, w.lanes, 1, 0, w.level, c.n, c.seed_weight, 2,
+                                          op.out.bundle, c.d_pc, c.stream));
+    c.count();
+    cur_comps[op.out.bundle] = 1;
+    return;
+  }
   for (const hp::LaneSlice& s : op.ins)
     if (shadow[s.bundle]) materialize(s.bundle);
   const bool defer = wrap_deferrable(op);
@@ -434,14 +525,19 @@ void Executor::step(const hp::HeOp& op, int64_t i) {
       S = c.new_bundle(s.lane_count, 2, L, true);
       shadow_level[op.out.bundle] = L;
     }
-    c.op_cadd(*S, 0, s.lane_count, in, LaneMap{s.lane, s.lane_count}, nullptr, LaneMap{0, 1}, L, true);
+    if (!o.shard) {
+      c.op_cadd(*S, 0, s.lane_count, in, LaneMap{s.lane, s.lane_count}, nullptr, LaneMap{0, 1}, L, true);
+    } else {  // the operand lanes this rank owns (the only ones its output lanes read)
+      for (auto [rs, re] : o.shard->runs(s.bundle, s.lane, s.lane_count))
+        c.op_cadd(*S, rs - s.lane, re - rs, in, LaneMap{rs, re - rs}, nullptr, LaneMap{0, 1}, L, true);
+    }
     get(op.out.bundle);  // the bundle exists from here on, as if written
     cur_comps[op.out.bundle] = 2;
     return;
   }
   if (op.kind == K::kPAdd) throw Error(AEGIS_ELOGIC, "PAdd is not emitted by the reference lowering");
   if (op.kind == K::kPMult) {
-    pmult(op);
+    pmult(op, i);
     cur_comps[op.out.bundle] = 2;
     return;
   }
@@ -460,7 +556,9 @@ void Executor::step(const hp::HeOp& op, int64_t i) {
           c.op_relin(get(op.out.bundle), op.out.lane + pos, len, L);
           break;
         case K::kRescale: {
-          Bundle& in = input(op.ins[0]);
+          // only the exchanges covering these lanes (the rest may still be in flight)
+          const LaneMap im = sub_map(op.ins[0], n, pos, len);
+          Bundle& in = im.count == len ? input(op.ins[0], im.lane0, im.lane0 + len) : input(op.ins[0]);
           c.op_rescale(get(op.out.bundle), op.out.lane + pos, in, sub_map(op.ins[0], n, pos, len), len, L);
           break;
         }

@@ -7,6 +7,7 @@
 
 #include "context.h"
 #include "heplan_ir.h"
+#include "p2p.h"
 #include "shard.h"
 
 namespace aegis {
@@ -28,6 +29,18 @@ struct RunOptions {
   const ShardPlan* hash_lanes = nullptr;
   ReduceFn reduce = nullptr;
   void* reduce_user = nullptr;
+  // device-synchronised reduce-scatter window (p2p.h): when set, sharded PCMM
+  // sums are exchanged on the comm stream as soon as the last PMult of the
+  // accumulator is issued, one exchange per sub-tensor, with CUDA-event edges
+  // back to the compute stream (no host callback, no host barrier)
+  P2pWindow* p2p = nullptr;
+  int fault = 0;  // fault injection (tests): 1 = drop the PCMM exchange (each rank keeps its partial sums)
+  // stored-plaintext PCMM (SURVEY §8(d) variant, §8(f) rank 4): every Encode op
+  // writes its weight bundle to HBM (kGenerate rows, 1 component) and the PMult
+  // kernel reads it instead of generating the weights in registers; every
+  // ciphertext bundle is bit-identical to the fused form (weight bundles are
+  // not hashed, as in the oracle, which never materialises them)
+  bool stored_weights = false;
   bool hoist = true;
   bool dce = false;  // skip output lanes no later op reads (final bundle unchanged)
   bool wrap_defer = true;  // wrapped accumulating CAdds summed at the operand's width (bit-identical)
@@ -39,7 +52,7 @@ class Executor {
   Executor(Context& c, const heplan::HeOpGraph& g, const RunOptions& opt);
   ~Executor();
   void run();
-  size_t h2d_bytes = 0, d2h_bytes = 0;
+  size_t h2d_bytes = 0, d2h_bytes = 0, comm_bytes = 0;
 
  private:
   struct Group {  // Rot ops sharing one source (hoisted ModUp)
@@ -55,7 +68,7 @@ class Executor {
   };
 
   Bundle& get(u32 id);
-  Bundle& input(const heplan::LaneSlice& s);
+  Bundle& input(const heplan::LaneSlice& s, u32 lo = 0, u32 hi = ~0u);
   void retire(u32 id);
   void hash_bundle(u32 id, const Bundle& b);
   void find_hoist_groups();
@@ -63,7 +76,11 @@ class Executor {
   bool live_lane(u32 b, u32 lane) const { return !o.dce || live[b][lane]; }
   size_t hoist_budget(size_t out_bytes);
   void step(const heplan::HeOp& op, int64_t i);
-  void pmult(const heplan::HeOp& op);
+  void pmult(const heplan::HeOp& op, int64_t i);
+  void reduce_async(u32 bundle);
+  // compute stream waits for the comm-stream exchanges of `bundle` that cover
+  // lanes [lo, hi) (all of them by default)
+  void wait_pending(u32 bundle, u32 lo = 0, u32 hi = ~0u);
   void rot_run(const heplan::HeOp& op, int64_t i, u32 r0, u32 len);
   void reduce_partial(u32 bundle);
   void donate(const heplan::HeOp& op, int64_t i);
@@ -78,8 +95,14 @@ class Executor {
   RunOptions o;
   std::vector<Bundle*> buf;
   std::vector<u32> alloc_comps, cur_comps;
-  std::vector<char> zero_first, partial, donated;
-  std::vector<int64_t> last_use;
+  std::vector<char> zero_first, partial, donated, is_weight;
+  std::vector<int64_t> last_use, last_pmult;
+  struct Pending {
+    u32 lo, hi;
+    cudaEvent_t ev;
+  };
+  std::vector<std::vector<Pending>> pending;  // comm-stream exchanges not yet waited for
+  std::vector<cudaEvent_t> events;            // every event this run created (destroyed at the end)
   std::vector<Group> groups;
   std::vector<int> group_of;
   std::vector<std::vector<char>> live;  // dce: [bundle][lane] read by a later op (or final)

@@ -510,7 +510,7 @@ inline u32 pmult_groups(u32 c_out) {
 // the per-iteration key fetch is an LDS broadcast, not a dependent LDG).
 // MINB: resident CTAs the register budget targets -- 3 when SMEM allows it
 // (TG = 4 then spills a few words, still the faster trade), else 2.
-template <int TG, int MINB>
+template <int TG, int MINB, bool STORED>
 __global__ void __launch_bounds__(256, MINB) pmult_kernel(const PmultArgs a, const PrimeConst* __restrict__ pc) {
   extern __shared__ Split xs[];
   const u32 n = a.n, c_in = a.c_in, c_out = a.c_out, limbs = a.limbs;
@@ -520,10 +520,11 @@ __global__ void __launch_bounds__(256, MINB) pmult_kernel(const PmultArgs a, con
   const PrimeConst P = pc[lb];
   const u32 nx = TG * c_in;
   u64* rks = reinterpret_cast<u64*>(xs + nx * 2 * kPmTx);
-  for (u32 e = threadIdx.x; e < c_in * c_out; e += blockDim.x) {
-    const u32 ci = e / c_out, o = e - ci * c_out;
-    rks[e] = a.rowkeys[(size_t)((a.ci_off + ci) * a.w_cout + a.o_off + o) * limbs + lb];
-  }
+  if (!STORED)
+    for (u32 e = threadIdx.x; e < c_in * c_out; e += blockDim.x) {
+      const u32 ci = e / c_out, o = e - ci * c_out;
+      rks[e] = a.rowkeys[(size_t)((a.ci_off + ci) * a.w_cout + a.o_off + o) * limbs + lb];
+    }
   for (u32 e = threadIdx.x; e < nx * 2 * kPmTx; e += blockDim.x) {
     const u32 xx = e % kPmTx, r = e / kPmTx, comp = r & 1, ln = r >> 1;
     const u32 t = ln / c_in, ci = ln - t * c_in;
@@ -545,7 +546,8 @@ __global__ void __launch_bounds__(256, MINB) pmult_kernel(const PmultArgs a, con
     Acc3 s[TG][2];
 #pragma unroll 1
     for (u32 ci = 0; ci < c_in; ++ci) {
-      const Split w = split24(uniform_at(rks[ci * c_out + o], xi, P.p, P.shift));
+      const Split w = STORED ? split24(a.wst.limb(a.w_lane0 + (a.ci_off + ci) * a.w_cout + a.o_off + o, 0, lb, n)[xi])
+                             : split24(uniform_at(rks[ci * c_out + o], xi, P.p, P.shift));
 #pragma unroll
       for (int t = 0; t < TG; ++t) {
         const u32 r = (t * c_in + ci) * 2;
@@ -753,13 +755,15 @@ cudaError_t launch_weight_rowkeys(u64* out, u32 wlanes, u32 limbs, u64 seed, u64
 cudaError_t launch_pmult_acc(const PmultArgs& a, const PrimeConst* pc, cudaStream_t st) {
   if (a.n < kPmTx) return cudaErrorInvalidValue;
   const u32 tg4 = a.tg < 4 ? a.tg : 4;
-  const size_t smem = ((size_t)tg4 * a.c_in * 2 * kPmTx + (size_t)a.c_in * a.c_out) * sizeof(u64);
+  const bool stored = a.wst.base != nullptr;
+  const size_t smem = ((size_t)tg4 * a.c_in * 2 * kPmTx + (stored ? 0 : (size_t)a.c_in * a.c_out)) * sizeof(u64);
   const unsigned grid = a.limbs * (a.n / kPmTx);
   const unsigned block = kPmTx * pmult_groups(a.c_out);
   if (!grid || !a.c_in || !a.c_out) return cudaSuccess;
 #define AEGIS_PM(TGV)                                                                          \
   case TGV: {                                                                                  \
-    auto kern = smem * 3 <= 220 * 1024 ? pmult_kernel<TGV, 3> : pmult_kernel<TGV, 2>;           \
+    auto kern = stored ? (smem * 3 <= 220 * 1024 ? pmult_kernel<TGV, 3, true> : pmult_kernel<TGV, 2, true>)    \
+                       : (smem * 3 <= 220 * 1024 ? pmult_kernel<TGV, 3, false> : pmult_kernel<TGV, 2, false>); \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     kern<<<grid, block, smem, st>>>(a, pc);                                        \
     break;                                                                                     \

@@ -88,6 +88,11 @@ struct PmultArgs {
   u32 x_lane0, x_tstride;
   u32 tg, c_in, c_out, ci_off, o_off, w_cout, limbs, n;
   const u64* rowkeys;
+  // stored-plaintext variant: when wst.base is
+  // set the weights are read from this 1-component bundle (lane = weight lane
+  // + w_lane0) instead of being generated in-kernel; rowkeys is then unused
+  View wst{nullptr, 0, 1, 0};
+  u32 w_lane0 = 0;
 };
 cudaError_t launch_pmult_acc(const PmultArgs& a, const PrimeConst* pc, cudaStream_t st);
 cudaError_t launch_weight_rowkeys(u64* out, u32 wlanes, u32 limbs, u64 seed, u64 bundle,

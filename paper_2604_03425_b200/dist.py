@@ -130,3 +130,43 @@ class P2pReducer:
         for h, _ in self.win.values():
             self.ctx.lib.aegis_p2p_destroy(h)
         self.win = {}
+
+
+def attach_p2p(ctx, graph, groups, part):
+    """The default multi-GPU data plane: one peer-memory window per rank, opened
+    over its token group through CUDA IPC (handles exchanged once, here), and
+    attached to the graph so every sharded PCMM exchange runs on the context's
+    comm stream with device-side flags -- no Python and no host barrier inside
+    graph.run().  Returns the window (keep it alive while the graph runs), or
+    None when no token group spans several ranks.  If any rank of the group
+    cannot map the windows, every rank of it gets None (decided collectively)
+    and the caller falls back to a reduce hook."""
+    nbytes = graph.p2p_bytes()
+    if nbytes == 0:
+        return None
+    g = groups[graph.shard_info()["tg_lo"]]
+    m = dist.get_world_size(g)
+    win, err = None, ""
+    try:
+        win = ctx.p2p_window(nbytes)
+    except Exception as e:  # noqa: BLE001 -- decided collectively below
+        err = repr(e)
+    handles = [None] * m
+    dist.all_gather_object(handles, (win.handle if win else b"", err), group=g)
+    err = next((e for _, e in handles if e), "")
+    if not err:
+        try:
+            win.open_ipc([h for h, _ in handles], part)
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)
+        errs = [None] * m
+        dist.all_gather_object(errs, err, group=g)
+        err = next((e for e in errs if e), "")
+    if err:
+        import sys
+        print(f"aegis: peer-memory windows unavailable ({err}); using a reduce hook", file=sys.stderr)
+        if win:
+            win.close()
+        return None
+    graph.set_p2p(win)
+    return win

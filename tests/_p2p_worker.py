@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from paper_2604_03425_b200 import Context  # noqa: E402
-from paper_2604_03425_b200.dist import P2pReducer, make_reducer, token_group_comms  # noqa: E402
+from paper_2604_03425_b200.dist import P2pReducer, attach_p2p, make_reducer, token_group_comms  # noqa: E402
 
 
 def main():
@@ -26,14 +26,20 @@ def main():
     g.set_shard(ws, rank)
     info = g.shard_info()
     groups, m = token_group_comms(ws, info["tg_total"])
-    red = P2pReducer(c, groups, rank % m)
-    if os.environ.get("P2P_REDUCER") == "collective":  # the torch.distributed path, for comparison
-        red.fallback = make_reducer(groups, rank % m)
-    g.set_reducer(red)
+    mode = os.environ.get("P2P_MODE", "device")
+    g.set_fault(int(os.environ.get("P2P_FAULT", "0")))
+    win, red = None, None
+    if mode == "device":  # the executor's own data plane: comm stream + flags in peer memory
+        win = attach_p2p(c, g, groups, rank % m)
+    else:
+        red = P2pReducer(c, groups, rank % m)
+        if mode == "collective":  # the torch.distributed path, for comparison
+            red.fallback = make_reducer(groups, rank % m)
+        g.set_reducer(red)
     h = g.run(hashes=True)
     hs = [None] * ws
     dist.all_gather_object(hs, h.tolist())
-    used = red.fallback is None and len(red.win) > 0
+    used = win is not None if mode == "device" else (red.fallback is None and len(red.win) > 0)
     if rank == 0:
         base = c.graph(kind=0, tokens=tokens).run(hashes=True)
         total = np.zeros_like(base)
@@ -42,7 +48,12 @@ def main():
         bad = int((total != base).sum())
         print(f"P2P_{'OK' if bad == 0 else 'MISMATCH'} bundles={len(base)} bad={bad} m={m} used_p2p={used}",
               flush=True)
-    red.close()
+    dist.barrier()  # no rank unmaps a window its peers may still read
+    if red:
+        red.close()
+    if win:
+        g.set_p2p(None)
+        win.close()
     dist.barrier()
     dist.destroy_process_group()
 

@@ -23,12 +23,26 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,tokens", [(8, 64), (16, 64)])
-def test_p2p_reduce_scatter_processes(world, tokens):
-    env = dict(os.environ, P2P_TOKENS=str(tokens))
+@pytest.mark.parametrize("world,tokens,mode", [(8, 64, "device"), (16, 64, "device"), (8, 64, "hook")])
+def test_p2p_reduce_scatter_processes(world, tokens, mode):
+    """mode device: the executor's comm-stream exchange with flags in the IPC
+    windows (no Python in the layer); hook: the host-synchronised reducer."""
+    env = dict(os.environ, P2P_TOKENS=str(tokens), P2P_MODE=mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "_p2p_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("P2P_")]
     assert line and line[0].startswith("P2P_OK") and "used_p2p=True" in line[0], r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_p2p_dropped_exchange_is_detected():
+    """Separate processes, device data plane, exchange dropped by fault
+    injection: the summed hashes must differ from the unsharded run."""
+    env = dict(os.environ, P2P_TOKENS="64", P2P_MODE="device", P2P_FAULT="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "8",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "_p2p_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("P2P_")]
+    assert line and line[0].startswith("P2P_MISMATCH"), r.stdout[-2000:]

@@ -210,3 +210,94 @@ def test_rot_hoisted_equals_separate_rotations(logn, level, lanes):
         sep.free()
     for b in hoisted + [x]:
         b.free()
+
+
+# ---------------------------------------------------------------------------
+# stored plaintexts and the wire format (SURVEY §8(d) stored variant, §8(f) rank 4)
+@pytest.mark.parametrize("logn,tg,c_in,c_out,level", [(10, 1, 2, 3, 3), (16, 2, 3, 4, 5)])
+def test_pmult_acc_stored_equals_generated(logn, tg, c_in, c_out, level):
+    """PCMM reading stored weights (aegis_pmult_acc_stored) is bit-identical to
+    the fused kernel that generates them in registers."""
+    c = ctx(logn)
+    n, wb = 1 << logn, 9
+    rng = np.random.default_rng(13)
+    X = rand_bundle(rng, tg * c_in, 2, level, n)
+    x = upload(c, X)
+    A0 = rand_bundle(rng, tg * c_out, 2, level, n)
+    fused, stored = upload(c, A0), upload(c, A0)
+    c.pmult_acc(fused, x, wb, c_in * c_out, level)
+    W = c.bundle(c_in * c_out, 1, level)
+    c.encode(W, wb, level)
+    c.pmult_acc_stored(stored, x, W, level)
+    assert (fused.download() == stored.download()).all()
+    for b in (x, fused, stored, W):
+        b.free()
+
+
+def test_stored_weights_graph_matches_oracle(golden_dir):
+    """The whole config-1 op sequence (N = 2^10) with every Encode written to HBM
+    and every PMult reading it: every ciphertext bundle hash equals the oracle's."""
+    from conftest import golden_graph
+    c, o = ctx(10), Oracle(10)
+    path = golden_graph("ffn_n10_t8", golden_dir)
+    g = c.load_graph(path)
+    g.set_stored_weights(True)
+    got = g.run(hashes=True)
+    want = o.run_graph(path)
+    assert (got == want).all()
+    g.set_stored_weights(False)
+
+
+def test_bundle_store_round_trip(tmp_path):
+    from paper_2604_03425_b200 import Context
+    c = ctx(10)
+    rng = np.random.default_rng(21)
+    X = rand_bundle(rng, 3, 2, 6, 1 << 10)
+    b = upload(c, X)
+    p = tmp_path / "b.aegs"
+    c.bundle_save(b, p)
+    r = c.bundle_load(p)
+    assert (r.lanes, r.comps, r.level) == (3, 2, 6)
+    assert (r.download() == X).all()
+    raw = bytearray(open(p, "rb").read())
+    raw[128 + 8 * 1000] ^= 1  # one flipped payload bit
+    open(tmp_path / "bad.aegs", "wb").write(raw)
+    with pytest.raises(ValueError, match="hash mismatch"):
+        c.bundle_load(tmp_path / "bad.aegs")
+    open(tmp_path / "short.aegs", "wb").write(bytes(raw[:len(raw) // 2]))
+    with pytest.raises(ValueError, match="truncated"):
+        c.bundle_load(tmp_path / "short.aegs")
+    other = Context(log_n=11)
+    with pytest.raises(ValueError, match="different ring"):
+        other.bundle_load(p)
+    with pytest.raises(ValueError, match="not a key"):
+        c.keys_load(1001, p)
+    for x in (b, r):
+        x.free()
+
+
+@pytest.mark.parametrize("logn", [10, 16])
+def test_key_store_round_trip(logn, tmp_path):
+    """A rotation key saved from one context and streamed into a fresh one
+    (different key seed) rotates exactly as the original."""
+    from paper_2604_03425_b200 import Context
+    c = ctx(logn)
+    level, off = 5, 3
+    c.keys_generate([1000 + off])
+    rng = np.random.default_rng(2)
+    X = rand_bundle(rng, 2, 2, level, 1 << logn)
+    x = upload(c, X)
+    ref = c.bundle(2, 2, level)
+    c.rot(ref, x, off, level)
+    p = tmp_path / "k.aegs"
+    c.keys_save(1000 + off, p)
+    c2 = Context(log_n=logn, seed_key=0x1234)
+    c2.keys_load(1000 + off, p)
+    x2 = upload(c2, X)
+    got = c2.bundle(2, 2, level)
+    c2.rot(got, x2, off, level)
+    assert (got.download() == ref.download()).all()
+    with pytest.raises(ValueError, match="different forms"):
+        c2.keys_load(0, p)  # a rotation key cannot become the relinearisation key
+    for b in (x, ref):
+        b.free()
