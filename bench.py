@@ -293,13 +293,19 @@ def run_aegis(args):
     c = Context(log_n=N_LOG, device=local)
     g = c.graph(kind=0, tokens=args.tokens, layers=args.layers)
     tg_total = -(-args.tokens // ((1 << N_LOG) // 2 // 64))
+    win = None
     if ws > 1:
-        from paper_2604_03425_b200.dist import P2pReducer, make_reducer, token_group_comms
+        from paper_2604_03425_b200.dist import P2pReducer, attach_p2p, make_reducer, token_group_comms
         g.set_shard(ws, rank)
         groups, m = token_group_comms(ws, tg_total)
-        if m > 1:  # PCMM reduce-scatter over peer memory (AEGIS_REDUCER=nccl: the NCCL collective)
-            nccl = os.environ.get("AEGIS_REDUCER", "p2p") == "nccl"
-            g.set_reducer(make_reducer(groups, rank % m) if nccl else P2pReducer(c, groups, rank % m))
+        if m > 1:
+            # default: the executor's own data plane (comm stream, peer-memory windows, device flags);
+            # AEGIS_REDUCER=hook: the host-synchronised peer-memory reducer; =nccl: ncclReduceScatter
+            mode = os.environ.get("AEGIS_REDUCER", "device")
+            if mode == "device":
+                win = attach_p2p(c, g, groups, rank % m)
+            if win is None:
+                g.set_reducer(make_reducer(groups, rank % m) if mode == "nccl" else P2pReducer(c, groups, rank % m))
     c.keys_generate(g.key_ids())
     c.sync()
     st = torch.cuda.ExternalStream(c.stream)
@@ -375,6 +381,25 @@ def run_aegis(args):
         others = {name: time_config(c, st, kind, tokens)
                   for name, kind, tokens in (("config1_ffn_T128", 1, 128), ("config2_layer_T512", 0, 512))}
 
+    # ---- the Aegis plan of this layer at 8 devices (host-side; events, bytes) ----
+    plan = None
+    try:
+        ps = g.plan(max(ws, 8)).summary()
+        plan = {k: ps[k] for k in ("world", "token_groups", "ranks_per_group", "events", "events_executed",
+                                   "bytes_total", "bytes_ffn", "bytes_attention", "bytes_reference_rule",
+                                   "matmuls_gather_chosen")}
+        plan["comm_bytes_this_rank_last_run"] = g.comm_bytes()
+        plan["note"] = ("PCMM reduce-scatter per sub-tensor when a token group spans several devices; attention "
+                        "is lane-local under the reference's pairing (no collective); bytes_reference_rule = "
+                        "the volume if each matmul used the mode comm_plan.hpp:226-238 picks")
+    except Exception as exc:
+        plan = {"error": str(exc)[:200]}
+
+    # ---- stored-plaintext PCMM variant (config 2 layer; weights written to / read from HBM) ----
+    stored = None
+    if ws == 1 and not args.no_configs:
+        stored = time_config(c, st, 0, 512, stored=True)
+
     # ---- roofline of the step's dominant kernel (timed live in the step) + the NTT metric ----
     roof = step_roofline(probe, ms, args.steps, g)
     roof["ntt"] = ntt_roofline(c, st)
@@ -399,19 +424,27 @@ def run_aegis(args):
             "peak_device_bytes": peak_bytes,
             "dce_variant": dce,
             "other_configs": others,
+            "stored_weights_variant": stored,
+            "plan": plan,
         }
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()
+        if win is not None:
+            g.set_p2p(None)
+            win.close()
         dist.destroy_process_group()
 
 
-def time_config(c, st, kind, tokens):
+def time_config(c, st, kind, tokens, stored=False):
     """One warm + one timed run of another BASELINE config on this context
-    (reported for reference; a failure here never costs the headline line)."""
+    (reported for reference; a failure here never costs the headline line).
+    stored: the PCMM weights are written to HBM by the Encode ops and read by
+    the PMult kernel (SURVEY §8(d) stored-plaintext variant)."""
     import torch
     try:
         go = c.graph(kind=kind, tokens=tokens, layers=1)
+        go.set_stored_weights(stored)
         c.keys_generate(go.key_ids())
         go.run()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -420,7 +453,10 @@ def time_config(c, st, kind, tokens):
         e1.record(st)
         e1.synchronize()
         go.free()
-        return {"value": e0.elapsed_time(e1) / 1e3, "unit": "s/layer", "steps": 1}
+        r = {"value": e0.elapsed_time(e1) / 1e3, "unit": "s/layer", "steps": 1}
+        if stored:
+            r["workload"] = f"config-{'2' if tokens == 512 else '?'} layer, T={tokens}, stored weights"
+        return r
     except Exception as exc:
         return {"error": str(exc)[:200]}
 
@@ -471,9 +507,13 @@ def step_roofline(probe, ms, steps, g):
         out.update({"achieved": None, "frac": None})
     out["traffic"] = None
     try:
+        # DRAM bytes / algorithmic bytes of every cfwd_a launch of one layer (ncu + the probe,
+        # same run, profiles/r02_cfwd_a_full.json), applied to this step's per-launch bytes
         prof = json.load(open(os.path.join(ROOT, "profiles", "r02_cfwd_a_full.json")))
-        out["traffic"] = prof["dram_bytes_per_launch"]
-        out["ncu"] = {k: prof[k] for k in prof if k != "dram_bytes_per_launch"}
+        if out.get("alg_bytes_per_launch"):
+            out["traffic"] = prof["traffic_over_algorithmic"] * out["alg_bytes_per_launch"]
+        out["traffic_over_algorithmic"] = prof["traffic_over_algorithmic"]
+        out["ncu_full"] = prof["full_capture_T2048_launch_3000"]
     except Exception:
         pass
     _, _, ops, _ = g.export()

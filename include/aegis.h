@@ -19,6 +19,13 @@
  * ELOGIC -> std::logic_error, others -> std::runtime_error.
  * Threading: one host thread per context; all work is asynchronous on the
  * context's compute stream; errors from the device surface at aegis_sync().
+ * The device-synchronised PCMM exchange (aegis_graph_set_p2p) is for one
+ * process per GPU (the deployment, tested with separate processes) or one
+ * process driving several GPUs (aegis_p2p_open_local).  Several contexts of
+ * ONE process on ONE device share a CUDA context: a device-synchronising call
+ * in one rank's thread (memory mapping, cudaFree) then waits for another
+ * rank's flag-waiting kernel -- use the reduce hook there.  A waiting kernel
+ * traps after 60 s, so such a misuse is an error, not a hang. 
  */
 #ifndef AEGIS_H
 #define AEGIS_H

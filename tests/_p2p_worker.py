@@ -39,6 +39,9 @@ def main():
     h = g.run(hashes=True)
     hs = [None] * ws
     dist.all_gather_object(hs, h.tolist())
+    sent = [None] * ws
+    dist.all_gather_object(sent, g.comm_bytes())
+    planned = sum(e["bytes_total"] for e in g.plan(ws).events() if e["executed"])
     used = win is not None if mode == "device" else (red.fallback is None and len(red.win) > 0)
     if rank == 0:
         base = c.graph(kind=0, tokens=tokens).run(hashes=True)
@@ -46,8 +49,8 @@ def main():
         for x in hs:
             total = total + np.array(x, dtype=np.uint64)
         bad = int((total != base).sum())
-        print(f"P2P_{'OK' if bad == 0 else 'MISMATCH'} bundles={len(base)} bad={bad} m={m} used_p2p={used}",
-              flush=True)
+        print(f"P2P_{'OK' if bad == 0 else 'MISMATCH'} bundles={len(base)} bad={bad} m={m} used_p2p={used} "
+              f"sent={sum(sent)} planned={planned}", flush=True)
     dist.barrier()  # no rank unmaps a window its peers may still read
     if red:
         red.close()

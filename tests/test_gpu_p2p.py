@@ -1,5 +1,7 @@
-"""PCMM reduce-scatter over CUDA IPC / NVLink peer memory (csrc/p2p.cu,
-dist.P2pReducer) in real separate processes on one GPU (same-device IPC):
+"""PCMM reduce-scatter over CUDA IPC / NVLink peer memory in real separate
+processes on one GPU (same-device IPC): the executor's own data plane (device
+mode: comm stream, pushes + flags in the windows, no host in the loop;
+dist.attach_p2p) and the host-synchronised hook (dist.P2pReducer).
 N = 2^11, T = 64 has 4 token groups (the T = 2048, N = 2^16 structure), so
 world 8 / 16 puts 2 / 4 ranks on each group.  Bundle hashes summed over the
 ranks must equal the unsharded run, with the peer-memory path actually used."""
@@ -34,6 +36,9 @@ def test_p2p_reduce_scatter_processes(world, tokens, mode):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("P2P_")]
     assert line and line[0].startswith("P2P_OK") and "used_p2p=True" in line[0], r.stdout[-2000:] + r.stderr[-2000:]
+    # the bytes the ranks actually sent are the plan's executed events (aegis_plan_*)
+    kv = dict(t.split("=") for t in line[0].split()[1:])
+    assert int(kv["sent"]) == int(kv["planned"]) > 0, line[0]
 
 
 def test_p2p_dropped_exchange_is_detected():
@@ -46,3 +51,4 @@ def test_p2p_dropped_exchange_is_detected():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("P2P_")]
     assert line and line[0].startswith("P2P_MISMATCH"), r.stdout[-2000:]
+    assert " sent=0 " in line[0], line[0]
