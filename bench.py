@@ -342,7 +342,7 @@ def run_aegis(args):
         ms = float(t.item())
 
     # ---- e2e: through the public API with host buffers (H2D input, D2H output) ----
-    e2e_ms, h2d, d2h = end_to_end(c, g, args, st, barrier)
+    e2e_ms, h2d, d2h = end_to_end(c, g, args, st, barrier) if not args.no_e2e else (float("nan"), 0, 0)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -581,6 +581,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dce", action="store_true", help="skip the dead-lane-elimination variant")
     ap.add_argument("--no-configs", action="store_true", help="skip the config-1/2 reference timings")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (e2e) run (profiling only)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
