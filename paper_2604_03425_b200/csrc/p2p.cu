@@ -87,6 +87,7 @@ __global__ void p2p_wait_kernel(const u64* flags, u32 base, u32 m, u32 self, u64
 // counts itself in; the last one stores `value` into flag `field` + self of
 // each peer window (release, system scope) and resets the counter.
 __device__ void signal_when_done(u64* counter, const PeerPtrs& peers, u32 m, u32 self, u32 field, u64 value) {
+  __threadfence_system();  // every thread's stores (local or to peer windows) ordered before the count
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {

@@ -1,0 +1,73 @@
+"""Real GELU / exp / inverse-sqrt on real CKKS ciphertexts (
+paper_2604_03425_b200/nonlinear.py): polynomial approximations evaluated with
+the library's GPU operators, decrypted and compared with NumPy.  The CPU part
+checks the approximations themselves."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2604_03425_b200.nonlinear import power_coeffs
+
+
+def _gelu(t):
+    return 0.5 * t * (1.0 + np.vectorize(math.erf)(t / math.sqrt(2.0)))
+
+
+def test_approximations_on_their_intervals():
+    u = np.linspace(-1, 1, 2001)
+    for f, lo, hi, deg, tol in ((_gelu, -4.0, 4.0, 16, 2e-3), (lambda t: np.exp(t / 4), -8.0, 0.0, 12, 1e-9),
+                                (lambda t: 1 / np.sqrt(t), 0.25, 4.0, 6, 5e-2)):
+        c = power_coeffs(f, lo, hi, deg)
+        x = 0.5 * (hi - lo) * u + 0.5 * (hi + lo)
+        assert np.abs(np.polynomial.polynomial.polyval(u, c) - f(x)).max() < tol
+
+
+@pytest.fixture(scope="module")
+def env():
+    from paper_2604_03425_b200 import Context
+    from paper_2604_03425_b200.boot import Bootstrapper
+    from paper_2604_03425_b200.ckks import Ckks
+    from paper_2604_03425_b200.nonlinear import Nonlinear
+    c = Context(log_n=10)
+    k = Ckks(c, seed=7, hamming=64)
+    k.upload_relin_key()
+    bs = Bootstrapper(c, k)
+    yield c, k, bs, Nonlinear(bs)
+    bs.close()
+
+
+def _run(env, fn, lo, hi, ref, level=30):
+    from paper_2604_03425_b200.boot import Ct
+    c, k, bs, nl = env
+    rng = np.random.default_rng(3)
+    x = rng.uniform(lo, hi, c.n // 2)
+    scale = 2.0 ** 40
+    ct = Ct(k.encrypt(x, scale, level), level, scale)
+    out = fn(nl, ct)
+    got = k.decrypt(out.b, out.scale, out.level).real
+    err = np.abs(got - ref(x)).max()
+    ct.free()
+    out.free()
+    return err, out.level
+
+
+@pytest.mark.gpu
+def test_gelu_on_ciphertexts(env):
+    err, lv = _run(env, lambda nl, ct: nl.gelu(ct), -4.0, 4.0, _gelu)
+    print(f"gelu: max error {err:.2e}, output level {lv}")
+    assert err < 3e-3
+
+
+@pytest.mark.gpu
+def test_exp_on_ciphertexts(env):
+    err, lv = _run(env, lambda nl, ct: nl.exp(ct), -8.0, 0.0, np.exp)
+    print(f"exp: max error {err:.2e}, output level {lv}")
+    assert err < 1e-4
+
+
+@pytest.mark.gpu
+def test_inv_sqrt_on_ciphertexts(env):
+    err, lv = _run(env, lambda nl, ct: nl.inv_sqrt(ct), 0.25, 4.0, lambda t: 1 / np.sqrt(t))
+    print(f"inv_sqrt: max error {err:.2e}, output level {lv}")
+    assert err < 1e-3
