@@ -185,6 +185,58 @@ class Ckks:
         self.ctx.ntt(bundle, lane=lane, lanes=1, lo=0, hi=level - 1)
         return bundle
 
+    def secret_bundle(self, level):
+        """The secret s as a 1-component NTT-domain bundle (cached per level): the
+        GPU-side encryption / decryption multiply by it with aegis_limb_op."""
+        cache = self.__dict__.setdefault("_s_dev", {})
+        if level not in cache:
+            b = self.ctx.bundle(1, 1, level)
+            b.upload(self._reduce_int(self.s, self.q[:level]).reshape(1, 1, level, self.n))
+            self.ctx.ntt(b)
+            cache[level] = b
+        return cache[level]
+
+    def encrypt_gpu(self, z, scale, level):
+        """The same symmetric encryption with the ring arithmetic on the GPU: the
+        host only samples (a uniform, e Gaussian) and encodes m; a * s, the sum and
+        the NTTs run as library kernels (aegis_ntt, aegis_limb_op)."""
+        from . import _lib as L
+        c = self.ctx
+        a = self._uniform(self.q[:level])
+        em = self._reduce_int(self.encode(z, scale) + self._error(), self.q[:level])
+        ct = c.bundle(1, 2, level)
+        host = np.zeros((1, 2, level, self.n), dtype=np.uint64)
+        host[0, 0], host[0, 1] = em, a
+        ct.upload(host)
+        c.ntt(ct)  # both components to the evaluation domain
+        a_pt = c.bundle(1, 1, level)  # component 1 (a) as a plaintext operand
+        a_pt.upload(host[:, 1:2])
+        c.ntt(a_pt)
+        prod = c.bundle(1, 1, level)
+        c.limb_op(L.LIMB_MUL, prod, a_pt, self.secret_bundle(level))  # a * s
+        c.limb_op(L.LIMB_SUB, ct, ct, prod, lanes=1)  # c0 = (e + m) - a s (plaintext b feeds comp 0)
+        a_pt.free()
+        prod.free()
+        return ct
+
+    def decrypt_gpu(self, bundle, scale, level, lane=0):
+        """c0 + c1 s and the inverse NTT on the GPU; CRT + decoding on the host."""
+        from . import _lib as L
+        c = self.ctx
+        m = c.bundle(1, 1, level)
+        c1 = c.bundle(1, 1, level)
+        h = bundle.download()[lane: lane + 1, :2, :level]
+        c1.upload(np.ascontiguousarray(h[:, 1:2]))
+        c0 = c.bundle(1, 1, level)
+        c0.upload(np.ascontiguousarray(h[:, 0:1]))
+        c.limb_op(L.LIMB_MUL, m, c1, self.secret_bundle(level))
+        c.limb_op(L.LIMB_ADD, m, m, c0)
+        c.ntt(m, inverse=True)
+        x = m.download()[0, 0]
+        for b in (m, c1, c0):
+            b.free()
+        return self.decode(self.crt(x, level), scale)
+
     def decrypt(self, bundle, scale, level, lane=0):
         """Slot vector of lane `lane` (first two components, `level` limbs)."""
         tmp = self.ctx.bundle(1, bundle.comps, bundle.level)

