@@ -372,6 +372,12 @@ int aegis_plan_events(const aegis_plan* p, aegis_plan_event* out, uint64_t cap, 
 int aegis_plan_device(const aegis_plan* p, uint32_t device, aegis_plan_instr* out, uint64_t cap, uint64_t* n);
 int aegis_plan_matmuls(const aegis_plan* p, aegis_plan_matmul* out, uint64_t cap, uint64_t* n);
 const char* aegis_plan_note(const aegis_plan* p);
+/* The graph as device `device` of the plan executes it: the same ops in the
+ * order of that device's compute stream (e.g. the staggered rotation-offset
+ * order of a reordered plan).  Only the order changes, and only inside a
+ * matmul's diagonal loop, whose accumulation commutes: every bundle is
+ * bit-identical.  Shard the new graph like the original. */
+int aegis_graph_from_plan(const aegis_graph* g, const aegis_plan* p, uint32_t device, aegis_graph** out);
 int aegis_plan_free(aegis_plan* p);
 /* bytes this rank sent through its PCMM exchanges in the last aegis_graph_run
  * (the executed counterpart of the plan's events) */

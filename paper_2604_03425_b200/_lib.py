@@ -149,6 +149,7 @@ SIGNATURES = [
     ("aegis_plan_device", ctypes.c_int, [vp, u32, ctypes.POINTER(AegisPlanInstr), u64, u64p]),
     ("aegis_plan_matmuls", ctypes.c_int, [vp, ctypes.POINTER(AegisPlanMatmul), u64, u64p]),
     ("aegis_plan_note", ctypes.c_char_p, [vp]),
+    ("aegis_graph_from_plan", ctypes.c_int, [vp, vp, u32, ctypes.POINTER(vp)]),
     ("aegis_plan_free", ctypes.c_int, [vp]),
     ("aegis_graph_comm_bytes", ctypes.c_int, [vp, u64p]),
     ("aegis_graph_owned_lanes", ctypes.c_int, [vp, u32, ctypes.POINTER(ctypes.c_uint8), u32]),

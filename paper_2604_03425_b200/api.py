@@ -418,6 +418,14 @@ class Graph:
             _raise(rc, self.lib.aegis_last_error(None).decode())
         return Plan(self.lib, h)
 
+    def in_plan_order(self, plan, device):
+        """This graph's ops in the order device `device` of `plan` runs them (bit-identical)."""
+        h = ctypes.c_void_p()
+        rc = self.lib.aegis_graph_from_plan(self.h, plan.h, device, ctypes.byref(h))
+        if rc:
+            _raise(rc, self.lib.aegis_last_error(None).decode())
+        return Graph(self.lib, h, self.ctx)
+
     def comm_bytes(self):
         """Bytes this rank sent through PCMM exchanges in the last run."""
         v = ctypes.c_uint64()

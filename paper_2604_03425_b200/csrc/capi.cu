@@ -948,6 +948,28 @@ int aegis_plan_matmuls(const aegis_plan* p, aegis_plan_matmul* out, uint64_t cap
   return AEGIS_OK;
 }
 const char* aegis_plan_note(const aegis_plan* p) { return p ? p->p.note.c_str() : ""; }
+int aegis_graph_from_plan(const aegis_graph* g, const aegis_plan* p, uint32_t device, aegis_graph** out) {
+  return guard(nullptr, [&] {
+    if (!g || !p || !out) throw Error(AEGIS_EINVAL, "graph_from_plan: null argument");
+    if (device >= p->p.devices.size()) throw Error(AEGIS_EINVAL, "graph_from_plan: no such device in the plan");
+    const auto& C = p->p.devices[device].compute;
+    std::vector<char> seen(g->g.ops.size(), 0);
+    auto ng = std::make_unique<aegis_graph>();
+    ng->g.bundles = g->g.bundles;
+    ng->g.graph_inputs = g->g.graph_inputs;
+    ng->header = g->header;
+    for (const aegis::PlanInstr& in : C) {
+      if (in.op >= g->g.ops.size()) throw Error(AEGIS_EINVAL, "graph_from_plan: plan does not belong to this graph");
+      if (seen[in.op]) continue;
+      seen[in.op] = 1;
+      ng->g.ops.push_back(g->g.ops[in.op]);
+    }
+    for (size_t i = 0; i < seen.size(); ++i)  // ops the device runs no lane of keep their place at the end
+      if (!seen[i]) ng->g.ops.push_back(g->g.ops[i]);
+    hp::validate_heops(ng->g);
+    *out = ng.release();
+  });
+}
 int aegis_plan_free(aegis_plan* p) {
   delete p;
   return AEGIS_OK;

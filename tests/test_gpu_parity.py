@@ -344,8 +344,9 @@ def test_graph_parity_small(name, logn, golden_dir):
     assert (g2.run(hashes=True) == h_gpu).all()
 
 
-@pytest.mark.parametrize("world,dce", [(2, False), (4, False), (8, False), (8, True)])
-def test_sharded_execution_matches(world, dce, tmp_path):
+@pytest.mark.parametrize("world,dce,stagger", [(2, False, False), (4, False, False), (8, False, False),
+                                               (8, True, False), (8, False, True)])
+def test_sharded_execution_matches(world, dce, stagger, tmp_path):
     """Token-group sharding on one GPU: the per-rank bundle
     hashes (owned lanes only) sum to the unsharded hashes.  N = 2^11, T = 64
     gives 4 token groups (score lanes >= output lanes, so attention stays
@@ -363,6 +364,9 @@ def test_sharded_execution_matches(world, dce, tmp_path):
     final = [int(ln.split()[4]) for ln in open(path) if ln.startswith("O ")][-1]
     ctxs = [Context(log_n=11) for _ in range(world)]
     graphs = [c_.graph(kind=0, tokens=64) for c_ in ctxs]
+    if stagger:  # each rank runs its own staggered diagonal order (aegis_graph_from_plan)
+        plan = graphs[0].plan(world, reorder=True)
+        graphs = [g.in_plan_order(plan, r) for r, g in enumerate(graphs)]
     for r, g in enumerate(graphs):
         g.set_shard(world, r)
         g.set_dce(dce)

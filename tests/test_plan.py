@@ -109,3 +109,26 @@ def test_unsplittable_shape_reports_why():
     assert s["executable"] == 0 and s["events"] == 0
     assert "reads lanes another rank owns" in p.note
     assert s["matmuls"] == 4 and s["bytes_reference_rule"] > 0
+
+
+def test_graph_in_plan_order_is_a_permutation(tmp_path):
+    """aegis_graph_from_plan: the ops of device d of a reordered plan, in that
+    device's order -- a permutation of the op list that moves only the
+    diagonal loops, each rotation still before its PMult."""
+    g = plan_graph(log_n=16, tokens=2048)
+    p = g.plan(8, reorder=True)
+    h = g.in_plan_order(p, 1)
+    a, b = tmp_path / "a.heops", tmp_path / "b.heops"
+    g.dump(a)
+    h.dump(b)
+    la = [ln for ln in open(a) if ln.startswith("O ")]
+    lb = [ln for ln in open(b) if ln.startswith("O ")]
+    assert sorted(la) == sorted(lb) and la != lb
+    ops = h.export()[2]
+    rot_pos = {}
+    for k, o in enumerate(ops):
+        if o.kind == 5:
+            rot_pos[o.out.bundle] = k
+        if o.kind == 3:  # PMult reads its rotated input after the rotation produced it
+            src = o.ins[0].bundle
+            assert src not in rot_pos or rot_pos[src] < k
