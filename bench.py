@@ -296,6 +296,9 @@ def run_aegis(args):
     win = None
     if ws > 1:
         from paper_2604_03425_b200.dist import P2pReducer, attach_p2p, make_reducer, token_group_comms
+        if ws > tg_total and os.environ.get("AEGIS_STAGGER", "1") == "1":
+            # this rank's staggered diagonal order from the Aegis plan (bit-identical)
+            g = g.in_plan_order(g.plan(ws, reorder=True), rank)
         g.set_shard(ws, rank)
         groups, m = token_group_comms(ws, tg_total)
         if m > 1:
