@@ -195,6 +195,41 @@ def test_rot(logn, level, offset):
         assert (got[ln] == exp).all(), ln
 
 
+@pytest.mark.parametrize("logn,level,offset", [(10, 3, 0), (10, 3, -499), (10, 2, 511), (10, 1, 5), (17, 5, 7)])
+def test_rot_edges(logn, level, offset):
+    """Edge offsets and shapes: offset 0 (galois 1: a plain key switch), the most
+    negative offset a key id allows (-499), N/2 - 1, level 1 (one digit of one
+    prime) and the N = 2^17 ring."""
+    c, o = ctx(logn), orc(logn)
+    n = 1 << logn
+    rng = np.random.default_rng(abs(offset) + level)
+    x = rand_bundle(rng, 2, 2, level, n)
+    bi = upload(c, x)
+    bo = c.bundle(2, 2, level)
+    c.rot(bo, bi, offset, level)
+    got = bo.download()
+    for ln in range(2):
+        assert (got[ln] == o.rotate(x[ln], level, offset)).all(), ln
+    with pytest.raises(ValueError):
+        c.rot(bo, bi, -500, level)  # key id 500 would collide with the relin id space
+
+
+def test_keyswitch_full_chain_60():
+    """A 60-prime chain (the config-5 sweep's context) at its top level: 15 digits,
+    64 extended slots -- the largest conversion and key product shapes."""
+    from paper_2604_03425_b200 import Context
+    from oracle_py import Oracle
+    c, o = Context(log_n=16, chain_length=60, bootstrap_level=14), Oracle(16, chain=60)
+    level = 60
+    rng = np.random.default_rng(60)
+    x = rand_bundle(rng, 1, 2, level, 1 << 16)
+    bi = upload(c, x)
+    bo = c.bundle(1, 2, level)
+    c.rot(bo, bi, 3, level)
+    assert (bo.download()[0] == o.rotate(x[0], level, 3)).all()
+    c.close()
+
+
 @pytest.mark.parametrize("logn,level", [(10, 4), (10, 16), (16, 3)])
 def test_cmult_relin(logn, level):
     c, o = ctx(logn), orc(logn)
