@@ -10,6 +10,8 @@ DESIGN.md §2.4 hash of every bundle, at N = 2^16 with the BERT parameters:
   prod_block_n16_t2048_tg0.json   the headline T = 2048 layer, the lanes of
                                   token group 0 of 4 (orc_run_graph_tg: the
                                   oracle's own token-coherent lane tagging)
+  prod_blocks2_n16_t512.json      two blocks at T = 512 (3,022 ops): block 2 at
+                                  the steady-state levels of config 4
 
 tests/test_gpu_parity.py compares every hash with the GPU executor's (the
 headline run is unsharded; it hashes the token-group-0 lanes only).
@@ -33,6 +35,8 @@ JOBS = {  # fixture -> (graph, tg_total, tg_sel)
     "prod_ffn_n16_t128": ("ffn_n16_t128", 1, -1),
     "prod_block_n16_t512": ("block_n16_t512", 1, -1),
     "prod_block_n16_t2048_tg0": ("block_n16_t2048", 4, 0),
+    # two blocks at T = 512: the second runs at the steady-state levels of config 4's blocks 2..12
+    "prod_blocks2_n16_t512": ("blocks2_n16_t512", 1, -1),
 }
 
 

@@ -452,7 +452,7 @@ def test_sharded_execution_matches(world, dce, stagger, tmp_path):
     assert len(bad) == 0, f"{len(bad)} bundles differ, first {bad[:5]}"
 
 
-PROD_FIXTURES = ["prod_ffn_n16_t128", "prod_block_n16_t512", "prod_block_n16_t2048_tg0"]
+PROD_FIXTURES = ["prod_ffn_n16_t128", "prod_block_n16_t512", "prod_block_n16_t2048_tg0", "prod_blocks2_n16_t512"]
 
 
 @pytest.mark.slow
