@@ -89,3 +89,44 @@ def test_gpu_side_encrypt_decrypt(env):
     assert np.abs(k.decrypt_gpu(ct2, scale, level) - z).max() < 1e-6
     for b in (ct, ct2):
         b.free()
+
+
+@pytest.mark.gpu
+def test_encrypted_mlp_block_with_bootstrap():
+    """A real encrypted MLP block end to end on the GPU operators, against NumPy
+    float64: y = W2 . bootstrap(gelu(W1 . x)).  W1, W2 are dense 512 x 512
+    matrices applied by BSGS over the slot diagonals, GELU is the degree-16
+    approximation, and the ciphertext is refreshed by real bootstrapping
+    (level 1 -> 21) before the second matmul."""
+    from paper_2604_03425_b200 import Context
+    from paper_2604_03425_b200.boot import Bootstrapper, Ct
+    from paper_2604_03425_b200.ckks import Ckks
+    from paper_2604_03425_b200.nonlinear import Nonlinear
+    c = Context(log_n=10)
+    k = Ckks(c, seed=13, hamming=64)
+    bs = Bootstrapper(c, k)
+    bs.upload_keys()
+    nl = Nonlinear(bs)
+    n = c.n // 2
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-1, 1, n)
+    W1 = rng.uniform(-1, 1, (n, n)) * (2.0 / np.sqrt(n))
+    W2 = rng.uniform(-1, 1, (n, n)) * (1.0 / np.sqrt(n))
+    want = W2 @ _gelu(W1 @ x)
+    scale = 2.0 ** 40
+    ct = Ct(k.encrypt(x, scale, 35), 35, scale)
+    h1 = bs.linear(ct, W1)                    # level 34
+    assert np.abs(W1 @ x).max() < 4.0         # inside GELU's approximation interval
+    g = nl.gelu(h1)
+    low = bs.mul_const(g, 1.0, 2.0 ** 34)     # same values at scale 2^34: q_0 / (Delta |m|) >= 2^10
+    one = bs.drop(low, 1)
+    fresh = bs.bootstrap(one.b, 2.0 ** 34)    # level 21
+    y = bs.linear(fresh, W2)
+    got = k.decrypt(y.b, y.scale, y.level).real
+    err = np.abs(got - want).max()
+    print(f"encrypted MLP block (matmul, GELU, bootstrap, matmul): max error {err:.2e}, "
+          f"|y| <= {np.abs(want).max():.2f}, output level {y.level}")
+    assert err < 2e-2
+    for t in (ct, h1, g, low, one, fresh, y):
+        t.free()
+    bs.close()
