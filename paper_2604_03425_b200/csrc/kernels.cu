@@ -120,6 +120,34 @@ __global__ void __launch_bounds__(256) cmult4_kernel(View out, u32 out_lane0, Vi
   st256cs(out.limb(out_lane0 + l, 2, lb, n) + x, d2[0], d2[1], d2[2], d2[3]);
 }
 
+// CMult of a ciphertext with itself (the softmax / GELU / LayerNorm squaring
+// chains, he_ir.hpp:305-322): (a0^2, 2 a0 a1, a1^2) -- 2 operand streams
+// instead of 4 (5 limb streams per limb instead of 7), 3 products instead of 4.
+__global__ void __launch_bounds__(256) square4_kernel(View out, u32 out_lane0, View a, LaneMap ma, u32 nlanes,
+                                                      u32 limbs, u32 n, const PrimeConst* __restrict__ pc) {
+  const u32 cpr = n / 1024;
+  const u32 row = blockIdx.x / cpr, chunk = blockIdx.x - row * cpr;
+  const u32 lb = row % limbs, l = row / limbs;
+  const PrimeConst P = pc[lb];
+  const u32 la = ma.at(l, nlanes);
+  const u32 x = (chunk * 256 + threadIdx.x) * 4;
+  u64 a0[4], a1[4];
+  ld256g(a.limb(la, 0, lb, n) + x, a0[0], a0[1], a0[2], a0[3]);
+  ld256g(a.limb(la, 1, lb, n) + x, a1[0], a1[1], a1[2], a1[3]);
+  u64 d0[4], d1[4], d2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d0[i] = mul_mod(a0[i], a0[i], P.p, P.mu104);
+    u128 s = mul_wide(a0[i], a1[i]);
+    mac(s, a1[i], a0[i]);
+    d1[i] = reduce104(s, P.p, P.mu104);
+    d2[i] = mul_mod(a1[i], a1[i], P.p, P.mu104);
+  }
+  st256cs(out.limb(out_lane0 + l, 0, lb, n) + x, d0[0], d0[1], d0[2], d0[3]);
+  st256cs(out.limb(out_lane0 + l, 1, lb, n) + x, d1[0], d1[1], d1[2], d1[3]);
+  st256cs(out.limb(out_lane0 + l, 2, lb, n) + x, d2[0], d2[1], d2[2], d2[3]);
+}
+
 // 8 contiguous coefficients per thread with 256-bit accesses (HBM-bound).
 // The accumulator / first operand streams (evict-first) so a wrapped second
 // operand (e.g. the 48 product lanes added into 1,536 score lanes) stays in L2.
@@ -612,7 +640,12 @@ cudaError_t launch_cmult(View out, u32 out_lane0, View a, LaneMap ma, View b, La
   if (n % 1024 == 0) {
     const size_t g = (size_t)nlanes * limbs * (n / 1024);
     if (!g) return cudaSuccess;
-    cmult4_kernel<<<(unsigned)g, 256, 0, st>>>(out, out_lane0, a, ma, b, mb, nlanes, limbs, n, pc);
+    const bool square = a.base == b.base && a.comps == b.comps && a.levels == b.levels && ma.lane0 == mb.lane0 &&
+                        ma.count == mb.count;
+    if (square)
+      square4_kernel<<<(unsigned)g, 256, 0, st>>>(out, out_lane0, a, ma, nlanes, limbs, n, pc);
+    else
+      cmult4_kernel<<<(unsigned)g, 256, 0, st>>>(out, out_lane0, a, ma, b, mb, nlanes, limbs, n, pc);
     return cudaGetLastError();
   }
   const u32 cpr = chunks_of(n);

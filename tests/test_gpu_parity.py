@@ -249,6 +249,27 @@ def test_cmult_relin(logn, level):
         assert (r[ln, :2] == o.relin(t[ln], level)).all()
 
 
+@pytest.mark.parametrize("logn,level", [(10, 4), (16, 7)])
+def test_cmult_square(logn, level):
+    """CMult of a ciphertext with itself takes the squaring kernel (2 operand
+    streams, 3 products); it must equal the general tensor product."""
+    c, o = ctx(logn), orc(logn)
+    rng = np.random.default_rng(level + 100)
+    a = rand_bundle(rng, 3, 2, level, 1 << logn)
+    ba = upload(c, a)
+    prod = c.bundle(3, 3, level)
+    c.cmult(prod, ba, ba, level)
+    t = prod.download()
+    for ln in range(3):
+        assert (t[ln] == o.cmult(a[ln], a[ln], level)).all()
+    # the same bundle with different lane slices is a general product
+    prod2 = c.bundle(2, 3, level)
+    c.cmult(prod2, ba, ba, level, lanes=2, a_slice=(0, 2), b_slice=(1, 2))
+    t2 = prod2.download()
+    for ln in range(2):
+        assert (t2[ln] == o.cmult(a[ln], a[ln + 1], level)).all()
+
+
 def test_cmult_lane_maps():
     """emit_per_lane wrap rule (he_ir.hpp:200-222): b lane = l % count."""
     c, o = ctx(10), orc(10)
