@@ -21,8 +21,9 @@ def main():
     rank, ws = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
     tokens = int(os.environ.get("P2P_TOKENS", "64"))
+    kind = int(os.environ.get("P2P_KIND", "0"))  # 1: the FFN graph (splittable at small T)
     c = Context(log_n=11)
-    g = c.graph(kind=0, tokens=tokens)
+    g = c.graph(kind=kind, tokens=tokens)
     g.set_shard(ws, rank)
     info = g.shard_info()
     groups, m = token_group_comms(ws, info["tg_total"])
@@ -44,7 +45,7 @@ def main():
     planned = sum(e["bytes_total"] for e in g.plan(ws).events() if e["executed"])
     used = win is not None if mode == "device" else (red.fallback is None and len(red.win) > 0)
     if rank == 0:
-        base = c.graph(kind=0, tokens=tokens).run(hashes=True)
+        base = c.graph(kind=kind, tokens=tokens).run(hashes=True)
         total = np.zeros_like(base)
         for x in hs:
             total = total + np.array(x, dtype=np.uint64)
