@@ -680,16 +680,26 @@ __device__ __forceinline__ void tile_cfwd_a(const NttLaunch& L, const NttConvIn&
     for (int i = 0; i <= K; ++i) w[i] = __ldg(ps[i] + (v << 12));
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      Acc3 a;
+      u64 r;
+      if constexpr (K == 1) {
+        // one source (rescale, boot from level 1): B = b_0, so [B/b_0]_t = 1 and
+        // the lift is x~ + v (d - [b_0]_d) -- no products; S < 2^48
+        const u64 S = (u64)w[0].x + ((u64)w[0].y << 24) +
+                      (w[1].x ? (u64)hs[t][1].lo + ((u64)hs[t][1].hi << 24) : 0ull);
+        const u64 q = __umul64hi(S >> 32, mu[t]);
+        r = S - q * dd[t];
+      } else {
+        Acc3 a;
 #pragma unroll
-      for (int i = 0; i < K; ++i) mac24(a, Split{w[i].x, w[i].y}, hs[t][i]);
-      // the overflow count v <= k has a zero high limb: two products, not four
-      a.c0 += (u64)w[K].x * hs[t][K].lo;
-      a.c1 += (u64)w[K].x * hs[t][K].hi;
-      // q = floor((S >> 32) floor(2^96/d) / 2^64) is within 3 below S/d: r = S - q d in [0, 3d)
-      const u64 top = (a.c2 << 16) + (a.c1 >> 8) + (a.c0 >> 32);
-      const u64 q = __umul64hi(top, mu[t]);
-      const u64 r = a.c0 + (a.c1 << 24) + (a.c2 << 48) - q * dd[t];
+        for (int i = 0; i < K; ++i) mac24(a, Split{w[i].x, w[i].y}, hs[t][i]);
+        // the overflow count v <= k has a zero high limb: two products, not four
+        a.c0 += (u64)w[K].x * hs[t][K].lo;
+        a.c1 += (u64)w[K].x * hs[t][K].hi;
+        // q = floor((S >> 32) floor(2^96/d) / 2^64) is within 3 below S/d: r = S - q d in [0, 3d)
+        const u64 top = (a.c2 << 16) + (a.c1 >> 8) + (a.c0 >> 32);
+        const u64 q = __umul64hi(top, mu[t]);
+        r = a.c0 + (a.c1 << 24) + (a.c2 << 48) - q * dd[t];
+      }
       if (t == 0) x[v] = u2d(r);
       else hand[(size_t)(t - 1) * 4096 + v * 256 + threadIdx.x] = r;
     }
