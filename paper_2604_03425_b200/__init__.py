@@ -4,7 +4,7 @@ The product is libaegis.so (hand-written sm_100a CUDA behind the C-ABI in
 include/aegis.h); this package is its thin Python host binding.
 """
 from .api import (BERT_PARAMS, SEED_INPUT, SEED_KEY, SEED_WEIGHT, AegisError, Bundle, Context,
-                  Graph, LogicError, plan_graph)
+                  Graph, LogicError, P2pWindow, Plan, graph_from_ops, plan_graph)
 
 __all__ = ["BERT_PARAMS", "SEED_INPUT", "SEED_KEY", "SEED_WEIGHT", "AegisError", "Bundle",
-           "Context", "Graph", "LogicError", "plan_graph"]
+           "Context", "Graph", "LogicError", "P2pWindow", "Plan", "graph_from_ops", "plan_graph"]
