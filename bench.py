@@ -300,6 +300,8 @@ def run_aegis(args):
             # this rank's staggered diagonal order from the Aegis plan (bit-identical)
             g = g.in_plan_order(g.plan(ws, reorder=True), rank)
         g.set_shard(ws, rank)
+        if os.environ.get("AEGIS_MATMUL_MODES") == "reference":  # gather where the reference's byte rule does
+            g.set_matmul_modes(True)
         groups, m = token_group_comms(ws, tg_total)
         if m > 1:
             # default: the executor's own data plane (comm stream, peer-memory windows, device flags);

@@ -333,6 +333,16 @@ int aegis_graph_set_p2p(aegis_graph* g, aegis_p2p* w);
  * ciphertext bundles are bit-identical to the default; weight bundles are not
  * hashed.  Default off. */
 int aegis_graph_set_stored_weights(aegis_graph* g, int enable);
+/* Matmul collective modes when a token group spans m > 1 devices.  0
+ * (default): every PCMM is input-stationary and reduce-scatters its partial
+ * outputs (no rotation is repeated).  1: each matmul takes the mode the
+ * reference's byte rule picks (comm_plan.hpp:226-238): where gathering the
+ * activation moves fewer bytes than reducing the outputs, the activation is
+ * all-gathered over the group on the comm stream and every rank rotates all
+ * of its lanes and computes its own output share completely.  Needs a p2p
+ * window (aegis_graph_set_p2p; size it with aegis_graph_p2p_bytes after this
+ * call); the plan (aegis_plan_build) follows the same modes.  Bit-identical. */
+int aegis_graph_set_matmul_modes(aegis_graph* g, int reference_rule);
 /* fault injection for tests: kind 1 drops the PCMM exchange (every rank keeps
  * its partial sums); 0 restores normal execution */
 int aegis_graph_set_fault(aegis_graph* g, int kind);

@@ -176,6 +176,7 @@ SIGNATURES = [
     ("aegis_graph_p2p_bytes", ctypes.c_int, [vp, u64p]),
     ("aegis_graph_set_p2p", ctypes.c_int, [vp, vp]),
     ("aegis_graph_set_fault", ctypes.c_int, [vp, ctypes.c_int]),
+    ("aegis_graph_set_matmul_modes", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_graph_set_stored_weights", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_pmult_acc_stored", ctypes.c_int, [vp, vp, u32, u32, u32, vp, u32, u32, vp, u32, u32, u32]),
 ]

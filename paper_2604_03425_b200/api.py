@@ -450,6 +450,10 @@ class Graph:
         """Stored-plaintext PCMM (weights written to HBM by the Encode ops, read by PMult)."""
         self.lib.aegis_graph_set_stored_weights(self.h, 1 if enable else 0)
 
+    def set_matmul_modes(self, reference_rule):
+        """1: each matmul gathers or reduces as the reference's byte rule picks (needs a p2p window)."""
+        self.lib.aegis_graph_set_matmul_modes(self.h, 1 if reference_rule else 0)
+
     def set_fault(self, kind):
         """Fault injection (tests): 1 drops the PCMM exchange, 0 restores it."""
         rc = self.lib.aegis_graph_set_fault(self.h, kind)

@@ -95,6 +95,7 @@ struct aegis_graph {
   aegis::P2pWindow* p2p = nullptr;  // device-synchronised exchange window (not owned)
   int fault = 0;
   int stored_weights = 0;
+  int reference_modes = 0;
   void* reduce_user = nullptr;
   int hoist = 1;
   int dce = 0;
@@ -126,6 +127,7 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.p2p = g->shard && g->shard->m > 1 ? g->p2p : nullptr;
   opt.fault = g->fault;
   opt.stored_weights = g->stored_weights != 0;
+  opt.reference_modes = g->reference_modes != 0;
   opt.hoist = g->hoist != 0;
   opt.dce = g->dce != 0;
   opt.wrap_defer = g->wrap_defer != 0;
@@ -885,7 +887,8 @@ int aegis_plan_build(const aegis_graph* g, uint32_t world, int reorder, aegis_pl
   return guard(nullptr, [&] {
     if (!g || !out || world == 0) throw Error(AEGIS_EINVAL, "plan_build: bad argument");
     auto pl = std::make_unique<aegis_plan>();
-    pl->p = aegis::build_plan(g->g, token_groups(g), world, (uint32_t)header_value(g->header, "N"), reorder != 0);
+    pl->p = aegis::build_plan(g->g, token_groups(g), world, (uint32_t)header_value(g->header, "N"), reorder != 0,
+                              g->reference_modes != 0);
     *out = pl.release();
   });
 }
@@ -993,6 +996,10 @@ int aegis_graph_p2p_bytes(const aegis_graph* g, uint64_t* bytes) {
                                                       acc.chunk_period);
         const uint64_t share = sh.c_sub / m;
         best = std::max<uint64_t>(best, share * std::max<uint32_t>(2, acc.components) * acc.level * n);
+        if (g->reference_modes) {  // the activation's share of a gather-mode matmul (up to 3 allocated comps)
+          const hp::CtBundle& x = g->g.bundles[op.ins[0].bundle];
+          best = std::max<uint64_t>(best, (uint64_t)(sh.c_in / m) * 3 * x.level * n);
+        }
       }
     }
     *bytes = 2 * (uint64_t)m * best * 8;  // two parities x m slots x the largest share
@@ -1024,6 +1031,11 @@ int aegis_pmult_acc_stored(aegis_ctx* ctx, aegis_bundle* acc, uint32_t acc_lane,
     ctx->c->op_pmult(A, acc_lane, acc_lanes, chunk_period, X, x_lane, x_lanes, 0, w_lanes, level, 0, ~0u, 0, ~0u, &W,
                      w_lane);
   });
+}
+int aegis_graph_set_matmul_modes(aegis_graph* g, int reference_rule) {
+  if (!g) return AEGIS_EINVAL;
+  g->reference_modes = reference_rule != 0;
+  return AEGIS_OK;
 }
 int aegis_graph_set_fault(aegis_graph* g, int kind) {
   if (!g || kind < 0 || kind > 1) return AEGIS_EINVAL;

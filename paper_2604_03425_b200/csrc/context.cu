@@ -936,7 +936,7 @@ void Context::op_cadd(Bundle& out, u32 out_lane, u32 lanes, const Bundle& a, Lan
 
 void Context::op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
                        u32 x_lanes, u32 wbundle, u32 wlanes, u32 level, u32 t_lo, u32 t_hi, u32 ci_lo,
-                       u32 ci_hi, const Bundle* wst, u32 w_lane0) {
+                       u32 ci_hi, const Bundle* wst, u32 w_lane0, u32 o_lo, u32 o_cnt) {
   const PcmmShape sh = pcmm_shape(x_lanes, acc_lanes, wlanes, chunk_period);
   t_hi = std::min(t_hi, sh.tg);
   ci_hi = std::min(ci_hi, sh.c_in);
@@ -953,16 +953,18 @@ void Context::op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_perio
     // sub-tensor s occupies acc lanes [s*chunk, (s+1)*chunk), token-major inside
     PmultArgs a;
     a.acc = acc.view();
-    a.acc_lane0 = acc_lane + pcmm_lane(sh, t_lo, s * sh.c_sub);
+    const u32 olo = std::min(o_lo, sh.c_sub), ocnt = std::min(o_cnt, sh.c_sub - olo);
+    if (!ocnt) continue;
+    a.acc_lane0 = acc_lane + pcmm_lane(sh, t_lo, s * sh.c_sub + olo);
     a.acc_tstride = sh.S == 1 ? sh.c_out : sh.c_sub;
     a.x = x.view();
     a.x_lane0 = x_lane + t_lo * sh.c_in + ci_lo;
     a.x_tstride = sh.c_in;
     a.tg = t_hi - t_lo;
     a.c_in = ci_hi - ci_lo;
-    a.c_out = sh.c_sub;
+    a.c_out = ocnt;
     a.ci_off = ci_lo;
-    a.o_off = s * sh.c_sub;
+    a.o_off = s * sh.c_sub + olo;
     a.w_cout = sh.c_out;
     a.limbs = level;
     a.n = n;

@@ -159,7 +159,8 @@ class Context {
   // step (defaults: everything); a position subset yields partial sums.
   void op_pmult(Bundle& acc, u32 acc_lane, u32 acc_lanes, u32 chunk_period, const Bundle& x, u32 x_lane,
                 u32 x_lanes, u32 wbundle, u32 wlanes, u32 level, u32 t_lo = 0, u32 t_hi = ~0u, u32 ci_lo = 0,
-                u32 ci_hi = ~0u, const Bundle* wstored = nullptr, u32 w_lane0 = 0);
+                u32 ci_hi = ~0u, const Bundle* wstored = nullptr, u32 w_lane0 = 0, u32 o_lo = 0,
+                u32 o_cnt = ~0u);  // outputs [o_lo, o_lo + o_cnt) of every sub-tensor
 
   void count(u64 k = 1) { launches += k; }
   // workspace budget of one operator phase: `gib` GiB scaled by AEGIS_WS_SCALE

@@ -14,6 +14,7 @@
 #include <set>
 
 #include "executor.h"
+#include "plan.h"
 
 namespace aegis {
 
@@ -49,6 +50,27 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
     }
   }
   if (o.shard && !o.shard->active()) o.shard = nullptr;
+  gather_acc.assign(nb, 0);
+  full_tg.assign(nb, 0);
+  gather_src.assign(nb, 0);
+  first_pmult.assign(nb, -1);
+  for (size_t i = 0; i < g.ops.size(); ++i)
+    if (g.ops[i].kind == hp::HeOpKind::kPMult && first_pmult[g.ops[i].out.bundle] < 0)
+      first_pmult[g.ops[i].out.bundle] = (int64_t)i;
+  if (o.reference_modes && o.shard && o.shard->m > 1) {
+    if (!o.p2p) throw Error(AEGIS_EINVAL, "matmul reference modes need a p2p window (aegis_graph_set_p2p)");
+    for (size_t b = 0; b < nb; ++b) {
+      if (first_pmult[b] < 0 || !gather_executed(g, (u32)b, (u32)first_pmult[b])) continue;
+      gather_acc[b] = 1;
+      const hp::HeOp& pm0 = g.ops[first_pmult[b]];
+      const u32 x = pm0.ins[0].bundle;
+      full_tg[x] = 1;
+      gather_src[x] = 1;
+      for (const hp::HeOp& op : g.ops)
+        if (op.kind == hp::HeOpKind::kRot && op.ins[0].bundle == x && op.app_node == pm0.app_node)
+          full_tg[op.out.bundle] = 1;
+    }
+  }
   if (o.hash_lanes && o.shard) throw Error(AEGIS_EINVAL, "hash lane selection applies to unsharded runs only");
   find_hoist_groups();
   if (o.dce) find_live_lanes();
@@ -124,6 +146,38 @@ Bundle& Executor::input(const hp::LaneSlice& s, u32 lo, u32 hi) {
   if (partial[s.bundle]) reduce_partial(s.bundle);
   if (!pending[s.bundle].empty()) wait_pending(s.bundle, lo, hi);
   return *buf[s.bundle];
+}
+
+// Gather-mode activation: the m ranks of the token group each computed their
+// own part of its lanes; one all-gather on the comm stream fills the rest.
+// Issued at the matmul's first read (the r = 0 PMult), waited on at once.
+void Executor::allgather(u32 x) {
+  gather_src[x] = 0;
+  const ShardPlan& P = *o.shard;
+  Bundle& X = *buf[x];
+  int64_t pm = -1;
+  for (size_t b = 0; b < g.bundles.size() && pm < 0; ++b)
+    if (gather_acc[b] && g.ops[first_pmult[b]].ins[0].bundle == x) pm = first_pmult[b];
+  const hp::HeOp& op = g.ops[pm];
+  const PcmmShape sh = pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count,
+                                  g.bundles[op.out.bundle].chunk_period);
+  if (sh.c_in % P.m) throw Error(AEGIS_EINVAL, "PCMM inputs do not split evenly over the ranks of a token group");
+  const size_t words_per_lane = (size_t)X.comps * X.level * c.n;
+  const size_t share = (size_t)(sh.c_in / P.m) * words_per_lane;
+  cudaEvent_t ready, done;
+  AEGIS_CHECK_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  AEGIS_CHECK_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  events.push_back(ready);
+  events.push_back(done);
+  AEGIS_CHECK_CUDA(cudaEventRecord(ready, c.stream));
+  AEGIS_CHECK_CUDA(cudaStreamWaitEvent(c.comm, ready, 0));
+  if (o.fault != 1) {
+    p2p_allgather(*o.p2p, X.view().limb(op.ins[0].lane + P.tg_lo * sh.c_in, 0, 0, c.n), share, c.comm);
+    c.count(4);
+    comm_bytes += (size_t)(P.m - 1) * share * 8;
+  }
+  AEGIS_CHECK_CUDA(cudaEventRecord(done, c.comm));
+  AEGIS_CHECK_CUDA(cudaStreamWaitEvent(c.stream, done, 0));
 }
 
 void Executor::wait_pending(u32 b, u32 lo, u32 hi) {
@@ -229,6 +283,7 @@ size_t Executor::hoist_budget(size_t out_bytes) {
 }
 
 void Executor::rot_run(const hp::HeOp& op, int64_t i, u32 pos, u32 len) {
+  if (full_tg[op.out.bundle] && gather_src[op.ins[0].bundle]) allgather(op.ins[0].bundle);
   Bundle& in = input(op.ins[0]);
   Bundle& out = get(op.out.bundle);
   const u32 L = op.use_level;
@@ -242,7 +297,8 @@ void Executor::rot_run(const hp::HeOp& op, int64_t i, u32 pos, u32 len) {
   const size_t per_lane = c.modup_words_per_lane(L);
   if (!gr.prepared) {
     gr.prepared = true;
-    gr.runs = o.shard ? o.shard->runs(gr.src, gr.lane0, gr.count)
+    gr.runs = o.shard ? (full_tg[gr.src] ? o.shard->tg_runs(gr.src, gr.lane0, gr.count)
+                                         : o.shard->runs(gr.src, gr.lane0, gr.count))
                       : std::vector<std::pair<u32, u32>>{{gr.lane0, gr.lane0 + gr.count}};
     if (o.dce && !gr.src_live.empty()) {  // only the source lanes some live rotation output needs
       std::vector<std::pair<u32, u32>> lr;
@@ -302,6 +358,8 @@ std::vector<std::pair<u32, u32>> Executor::out_runs(const hp::HeOp& op) const {
   std::vector<std::pair<u32, u32>> r;
   if (!o.shard) {
     r.emplace_back(0, n);
+  } else if (full_tg[op.out.bundle]) {  // gather-mode rotations: every lane of the token group
+    for (auto [s, e] : o.shard->tg_runs(op.out.bundle, op.out.lane, n)) r.emplace_back(s - op.out.lane, e - op.out.lane);
   } else {
     for (auto [s, e] : o.shard->runs(op.out.bundle, op.out.lane, n)) r.emplace_back(s - op.out.lane, e - op.out.lane);
   }
@@ -333,6 +391,7 @@ LaneMap Executor::sub_map(const hp::LaneSlice& s, u32 n, u32 pos, u32 len) {
 
 void Executor::pmult(const hp::HeOp& op, int64_t i) {
   if (!op.accumulate || op.ins.size() != 2) throw Error(AEGIS_ELOGIC, "unsupported PMult form");
+  if (gather_acc[op.out.bundle] && gather_src[op.ins[0].bundle]) allgather(op.ins[0].bundle);
   Bundle& x = input(op.ins[0]);
   Bundle& acc = get(op.out.bundle);
   const u32 chunk = g.bundles[op.out.bundle].chunk_period;
@@ -345,6 +404,14 @@ void Executor::pmult(const hp::HeOp& op, int64_t i) {
     return;
   }
   const ShardPlan& P = *o.shard;
+  if (P.m > 1 && gather_acc[op.out.bundle]) {
+    // output-stationary: all inputs of the group, this rank's share of every sub-tensor
+    const PcmmShape sh = pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count, chunk);
+    const u32 share = sh.c_sub / P.m;
+    c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
+               op.ins[1].lane_count, L, P.tg_lo, P.tg_lo + 1, 0, ~0u, ws, wl0, P.part * share, share);
+    return;
+  }
   if (P.m == 1) {
     c.op_pmult(acc, op.out.lane, op.out.lane_count, chunk, x, op.ins[0].lane, op.ins[0].lane_count, op.ins[1].bundle,
                op.ins[1].lane_count, L, P.tg_lo, P.tg_hi, 0, ~0u, ws, wl0);

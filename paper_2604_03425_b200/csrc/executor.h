@@ -41,6 +41,12 @@ struct RunOptions {
   // ciphertext bundle is bit-identical to the fused form (weight bundles are
   // not hashed, as in the oracle, which never materialises them)
   bool stored_weights = false;
+  // reference_modes (needs `p2p`): a matmul whose activation is cheaper to
+  // gather than its partial outputs are to reduce (plan.h gather_executed) runs
+  // output-stationary: the activation is all-gathered over the token group on
+  // the comm stream, every rank rotates all of its lanes and computes its own
+  // output share completely -- no reduction (comm_plan.hpp:226-238 kGatherInputs)
+  bool reference_modes = false;
   bool hoist = true;
   bool dce = false;  // skip output lanes no later op reads (final bundle unchanged)
   bool wrap_defer = true;  // wrapped accumulating CAdds summed at the operand's width (bit-identical)
@@ -78,6 +84,7 @@ class Executor {
   void step(const heplan::HeOp& op, int64_t i);
   void pmult(const heplan::HeOp& op, int64_t i);
   void reduce_async(u32 bundle);
+  void allgather(u32 bundle);  // gather-mode activation: all lanes of the token group
   // compute stream waits for the comm-stream exchanges of `bundle` that cover
   // lanes [lo, hi) (all of them by default)
   void wait_pending(u32 bundle, u32 lo = 0, u32 hi = ~0u);
@@ -96,6 +103,8 @@ class Executor {
   std::vector<Bundle*> buf;
   std::vector<u32> alloc_comps, cur_comps;
   std::vector<char> zero_first, partial, donated, is_weight;
+  std::vector<char> gather_acc, full_tg, gather_src;  // reference_modes bookkeeping (see RunOptions)
+  std::vector<int64_t> first_pmult;
   std::vector<int64_t> last_use, last_pmult;
   struct Pending {
     u32 lo, hi;

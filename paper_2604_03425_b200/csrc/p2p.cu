@@ -104,14 +104,16 @@ __device__ void signal_when_done(u64* counter, const PeerPtrs& peers, u32 m, u32
   if (threadIdx.x == 0) *counter = 0;
 }
 
-// blockIdx.y = target rank q: src share q -> window_q data slot (parity, self)
+// blockIdx.y = target rank q: src share q (all-gather: my own share, to every
+// peer) -> window_q data slot (parity, self)
+template <bool GATHER>
 __global__ void __launch_bounds__(256) p2p_push_kernel(const PeerPtrs peers, const u64* src, u32 m, u32 self,
                                                        size_t share, size_t slot_words, u32 parity, u64* counter,
                                                        u64 epoch) {
   const u32 q = blockIdx.y;
   if (q != self) {
     u64* dst = P2pWindow::data(peers.w[q]) + ((size_t)parity * m + self) * slot_words;
-    const u64* s = src + (size_t)q * share;
+    const u64* s = src + (size_t)(GATHER ? self : q) * share;
     for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < share;
          i += (size_t)gridDim.x * blockDim.x * 4) {
       u64 a, b, c, d;
@@ -141,6 +143,22 @@ __global__ void __launch_bounds__(256) p2p_sum_kernel(const PeerPtrs peers, u64*
     }
     st256g(mine + i, s0, s1, s2, s3);
   }
+  signal_when_done(counter, peers, m, self, kFlagAck, epoch);
+}
+
+// all-gather receive: share r of buf <- the slot peer r pushed into my window
+__global__ void __launch_bounds__(256) p2p_collect_kernel(const PeerPtrs peers, u64* buf, u32 m, u32 self,
+                                                          size_t share, size_t slot_words, u32 parity, u64* counter,
+                                                          u64 epoch) {
+  const u64* slots = P2pWindow::data(peers.w[self]) + (size_t)parity * m * slot_words;
+  const u32 r = blockIdx.y;
+  if (r != self)
+    for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < share;
+         i += (size_t)gridDim.x * blockDim.x * 4) {
+      u64 a, b, c, d;
+      ld256g(slots + (size_t)r * slot_words + i, a, b, c, d);
+      st256g(buf + (size_t)r * share + i, a, b, c, d);
+    }
   signal_when_done(counter, peers, m, self, kFlagAck, epoch);
 }
 
@@ -257,10 +275,29 @@ void p2p_exchange(P2pWindow& w, u64* buf, size_t share, cudaStream_t st) {
   // the slot (parity) this push overwrites was last read at epoch e - 2
   if (e > 2) p2p_wait_kernel<<<1, 32, 0, st>>>(fl, kFlagAck, m, w.self, e - 2);
   const unsigned bx = (unsigned)std::min<size_t>(256, std::max<size_t>(1, share / 1024));
-  p2p_push_kernel<<<dim3(bx, m), 256, 0, st>>>(pw, buf, m, w.self, share, slot, parity, fl + kFlagCount, e);
+  p2p_push_kernel<false><<<dim3(bx, m), 256, 0, st>>>(pw, buf, m, w.self, share, slot, parity, fl + kFlagCount, e);
   p2p_wait_kernel<<<1, 32, 0, st>>>(fl, kFlagReady, m, w.self, e);
   p2p_sum_kernel<<<bx, 256, 0, st>>>(pw, buf + (size_t)w.self * share, m, w.self, share, slot, parity,
                                      fl + kFlagCount + 1, e);
+  AEGIS_CHECK_CUDA(cudaGetLastError());
+}
+
+void p2p_allgather(P2pWindow& w, u64* buf, size_t share, cudaStream_t st) {
+  const u32 m = (u32)w.peers.size();
+  if (m < 2) throw Error(AEGIS_ELOGIC, "p2p_allgather: window not opened for a group");
+  if (share % 4 || reinterpret_cast<uintptr_t>(buf) % 32)
+    throw Error(AEGIS_EINVAL, "p2p_allgather: shares must be 32-byte aligned whole 4-word groups");
+  const size_t slot = p2p_capacity(w);
+  if (share > slot) throw Error(AEGIS_EINVAL, "p2p_allgather: share larger than the window slot");
+  const u64 e = ++w.epoch;
+  const u32 parity = (u32)(e & 1);
+  const PeerPtrs pw = peer_ptrs(w);
+  u64* fl = P2pWindow::flags(w.own);
+  if (e > 2) p2p_wait_kernel<<<1, 32, 0, st>>>(fl, kFlagAck, m, w.self, e - 2);
+  const unsigned bx = (unsigned)std::min<size_t>(256, std::max<size_t>(1, share / 1024));
+  p2p_push_kernel<true><<<dim3(bx, m), 256, 0, st>>>(pw, buf, m, w.self, share, slot, parity, fl + kFlagCount, e);
+  p2p_wait_kernel<<<1, 32, 0, st>>>(fl, kFlagReady, m, w.self, e);
+  p2p_collect_kernel<<<dim3(bx, m), 256, 0, st>>>(pw, buf, m, w.self, share, slot, parity, fl + kFlagCount + 1, e);
   AEGIS_CHECK_CUDA(cudaGetLastError());
 }
 

@@ -42,6 +42,10 @@ void p2p_reduce(Context& c, P2pWindow& w, u64* dst, size_t words_per_rank, u32 p
 // and acknowledges to every pusher so the slot can be reused two epochs later.
 // Every rank of the group must issue the same sequence of exchanges.
 void p2p_exchange(P2pWindow& w, u64* buf, size_t share, cudaStream_t st);
+// All-gather with the same window protocol: buf holds m shares of `share`
+// words; this rank's share (buf + self*share) is pushed to every peer and the
+// m-1 others land in place.  Every rank issues the same exchange sequence.
+void p2p_allgather(P2pWindow& w, u64* buf, size_t share, cudaStream_t st);
 // words of `share` one exchange can carry through this window
 size_t p2p_capacity(const P2pWindow& w);
 

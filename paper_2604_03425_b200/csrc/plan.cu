@@ -20,7 +20,15 @@ CommCategory category_of(const std::string& tag) {  // comm_plan.hpp:36-49 by ap
   return CommCategory::kOther;
 }
 
-ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, uint32_t ring_degree, bool reorder) {
+bool gather_executed(const hp::HeOpGraph& g, uint32_t acc, uint32_t first_pmult_op) {
+  const hp::HeOp& pm = g.ops[first_pmult_op];
+  const PcmmShape sh = pcmm_shape(pm.ins[0].lane_count, pm.out.lane_count, pm.ins[1].lane_count,
+                                  g.bundles[acc].chunk_period);
+  return (uint64_t)sh.c_in * g.bundles[pm.ins[0].bundle].level <= (uint64_t)sh.c_out * g.bundles[acc].level;
+}
+
+ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, uint32_t ring_degree, bool reorder,
+                    bool reference_modes) {
   if (world == 0 || tg_total == 0) throw std::invalid_argument("plan: world and token groups must be positive");
   ExecPlan P;
   P.world = world;
@@ -49,6 +57,23 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
     }
   }
 
+  // gather-mode matmuls (reference_modes): the activation and its rotations are
+  // computed on every lane of the token group, each device its own output share
+  std::vector<char> gather(g.bundles.size(), 0), full_tg(g.bundles.size(), 0), cmult_out(g.bundles.size(), 0);
+  for (const hp::HeOp& op : g.ops)
+    if (op.kind == K::kCMult) cmult_out[op.out.bundle] = 1;
+  if (reference_modes && P.m > 1 && P.executable)
+    for (size_t b = 0; b < g.bundles.size(); ++b) {
+      if (first_pmult[b] < 0 || !gather_executed(g, (uint32_t)b, (uint32_t)first_pmult[b])) continue;
+      gather[b] = 1;
+      const hp::HeOp& pm0 = g.ops[first_pmult[b]];
+      const uint32_t x = pm0.ins[0].bundle;
+      full_tg[x] = 1;
+      for (const hp::HeOp& op : g.ops)
+        if (op.kind == K::kRot && op.ins[0].bundle == x && op.app_node == pm0.app_node) full_tg[op.out.bundle] = 1;
+    }
+  auto comps_alloc = [&](uint32_t b) { return cmult_out[b] ? 3u : std::max(2u, g.bundles[b].components); };
+
   // ---- compute streams ------------------------------------------------------
   P.devices.resize(P.executable ? world : 0);
   std::vector<std::map<int64_t, uint32_t>> first_pos(world), last_pos(world);  // op -> compute position
@@ -60,6 +85,17 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
       uint8_t flags = 0;
       if (world == 1 || op.kind == K::kEncode) {
         runs.emplace_back(op.out.lane, op.out.lane + op.out.lane_count);
+      } else if (op.kind == K::kPMult && P.m > 1 && gather[op.out.bundle]) {
+        // every input of the group, this device's share of every sub-tensor's outputs
+        const PcmmShape sh = pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count,
+                                        g.bundles[op.out.bundle].chunk_period);
+        const uint32_t share = sh.c_sub / P.m;
+        for (uint32_t s = 0; s < sh.S; ++s) {
+          const uint32_t l0 = op.out.lane + pcmm_lane(sh, sp[d].tg_lo, s * sh.c_sub + sp[d].part * share);
+          runs.emplace_back(l0, l0 + share);
+        }
+      } else if (full_tg[op.out.bundle]) {
+        runs = sp[d].tg_runs(op.out.bundle, op.out.lane, op.out.lane_count);
       } else if (op.kind == K::kPMult && P.m > 1) {
         // input-stationary partial sums into every output lane of the group
         const PcmmShape sh = pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count,
@@ -105,12 +141,51 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
       mi.gather_bytes = (uint64_t)tg_total * (m - 1) * sh.c_in * ship_level * 2 * limb;
       mi.reduce_bytes = (uint64_t)tg_total * (m - 1) * sh.c_out * level * 2 * limb;
       mi.chosen = mi.gather_bytes <= mi.reduce_bytes ? MatmulMode::kGatherInputs : MatmulMode::kReduceOutputs;
-      mi.executed = P.executable ? MatmulMode::kReduceOutputs : MatmulMode::kLocal;
+      mi.executed = !P.executable ? MatmulMode::kLocal
+                    : gather[b]       ? MatmulMode::kGatherInputs
+                                      : MatmulMode::kReduceOutputs;
       // the rescale (first reader after the last PMult) waits for the exchange
       int64_t reader = -1;
       for (size_t i = (size_t)last_pmult[b] + 1; i < g.ops.size() && reader < 0; ++i)
         for (const hp::LaneSlice& s : g.ops[i].ins)
           if (s.bundle == b) reader = (int64_t)i;
+      if (gather[b]) {  // one AllGather of the activation per token group
+        const uint32_t x = pm0.ins[0].bundle;
+        int64_t producer_op = -1;  // the last writer of x before the matmul
+        for (int64_t i = 0; i < first_pmult[b]; ++i)
+          if (g.ops[i].out.bundle == x && g.ops[i].kind != K::kEncode) producer_op = i;
+        for (uint32_t t = 0; t < tg_total; ++t) {
+          PlanEvent e;
+          e.id = (uint32_t)P.events.size();
+          e.kind = CollKind::kAllGather;
+          e.semantic = CollSemantic::kMove;
+          e.dev_lo = t * m;
+          e.dev_count = m;
+          e.bundle = x;
+          e.lane = pm0.ins[0].lane + t * sh.c_in;
+          e.lane_count = sh.c_in;
+          e.level = g.bundles[x].level;
+          e.comps = comps_alloc(x);
+          e.bytes_per_device = (uint64_t)(m - 1) * (sh.c_in / m) * e.level * e.comps * limb;
+          e.bytes_total = e.bytes_per_device * m;
+          e.app_node = pm0.app_node;
+          e.he_op = producer_op >= 0 ? (uint32_t)producer_op : 0;
+          e.category = category_of(g.bundles[b].tag);
+          e.executed = true;
+          for (uint32_t dd = e.dev_lo; dd < e.dev_lo + m; ++dd) {
+            e.trigger_pos.push_back(producer_op >= 0 && last_pos[dd].count(producer_op) ? last_pos[dd].at(producer_op)
+                                                                                        : 0);
+            const uint32_t w = first_pos[dd].count(first_pmult[b]) ? first_pos[dd].at(first_pmult[b]) : UINT32_MAX;
+            e.wait_pos.push_back(w);
+            if (w != UINT32_MAX && P.devices[dd].compute[w].wait_event < 0)
+              P.devices[dd].compute[w].wait_event = (int32_t)e.id;
+            P.devices[dd].comm.push_back(e.id);
+          }
+          P.events.push_back(e);
+        }
+        P.matmuls.push_back(mi);
+        continue;
+      }
       for (uint32_t t = 0; t < (P.executable ? tg_total : 0); ++t)
         for (uint32_t s = 0; s < sh.S; ++s) {
           PlanEvent e;

@@ -86,8 +86,15 @@ struct ExecPlan {
   std::vector<MatmulInfo> matmuls;
 };
 
+// reference_modes: run each matmul in the mode the reference's byte rule picks
+// (gather the activation when that moves fewer bytes than reducing the
+// outputs; the activation itself is shipped, not a pre-boot form) -- the
+// executor's aegis_graph_set_matmul_modes(g, 1); otherwise always reduce
 ExecPlan build_plan(const heplan::HeOpGraph& g, uint32_t tg_total, uint32_t world, uint32_t ring_degree,
-                    bool reorder);
+                    bool reorder, bool reference_modes = false);
+// the executed choice for the accumulator `acc` when reference_modes is on:
+// gather iff c_in * level(activation) <= c_out * level(acc)
+bool gather_executed(const heplan::HeOpGraph& g, uint32_t acc, uint32_t first_pmult_op);
 CommCategory category_of(const std::string& bundle_tag);
 
 }  // namespace aegis

@@ -47,6 +47,21 @@ std::vector<std::pair<uint32_t, uint32_t>> ShardPlan::runs(uint32_t b, uint32_t 
   return r;
 }
 
+std::vector<std::pair<uint32_t, uint32_t>> ShardPlan::tg_runs(uint32_t b, uint32_t lane0, uint32_t count) const {
+  std::vector<std::pair<uint32_t, uint32_t>> r;
+  auto in = [&](uint32_t l) { return !active() || owns_tg(tags[b][l].tg); };
+  uint32_t i = lane0;
+  const uint32_t end = lane0 + count;
+  while (i < end) {
+    while (i < end && !in(i)) ++i;
+    if (i >= end) break;
+    const uint32_t s = i;
+    while (i < end && in(i)) ++i;
+    r.emplace_back(s, i);
+  }
+  return r;
+}
+
 ShardPlan make_shard_plan(const heplan::HeOpGraph& g, uint32_t tg_total, uint32_t world, uint32_t rank) {
   using K = heplan::HeOpKind;
   if (world == 0 || rank >= world || tg_total == 0) throw std::invalid_argument("bad shard spec");

@@ -40,6 +40,9 @@ struct ShardPlan {
   bool owns_tg(int32_t tg) const { return tg >= (int32_t)tg_lo && tg < (int32_t)tg_hi; }
   // maximal contiguous runs [start, end) of owned lanes inside [lane0, lane0 + count)
   std::vector<std::pair<uint32_t, uint32_t>> runs(uint32_t b, uint32_t lane0, uint32_t count) const;
+  // the same over every lane of this rank's token groups (all m parts): the
+  // lanes a gather-mode PCMM computes on every rank of the group
+  std::vector<std::pair<uint32_t, uint32_t>> tg_runs(uint32_t b, uint32_t lane0, uint32_t count) const;
 };
 
 // Tags every bundle lane; throws std::logic_error if an op mixes token groups

@@ -29,6 +29,7 @@ def main():
     groups, m = token_group_comms(ws, info["tg_total"])
     mode = os.environ.get("P2P_MODE", "device")
     g.set_fault(int(os.environ.get("P2P_FAULT", "0")))
+    g.set_matmul_modes(os.environ.get("P2P_MODES", "0") == "1")  # before the window is sized
     win, red = None, None
     if mode == "device":  # the executor's own data plane: comm stream + flags in peer memory
         win = attach_p2p(c, g, groups, rank % m)

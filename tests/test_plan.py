@@ -132,3 +132,26 @@ def test_graph_in_plan_order_is_a_permutation(tmp_path):
         if o.kind == 3:  # PMult reads its rotated input after the rotation produced it
             src = o.ins[0].bundle
             assert src not in rot_pos or rot_pos[src] < k
+
+
+def test_reference_modes_plan_gathers_where_the_rule_says():
+    """aegis_graph_set_matmul_modes(g, 1): qkv and ffn1 (activation cheaper to
+    ship than the partial outputs) become one AllGather per token group, out_proj
+    and ffn2 stay reduce-scatters; the plan moves fewer bytes, and every device
+    computes its own output share of a gathered matmul on all the group's inputs."""
+    g = plan_graph(log_n=16, tokens=2048)
+    base = g.plan(8, reorder=False).summary()
+    g.set_matmul_modes(True)
+    p = g.plan(8, reorder=False)
+    s, ev = p.summary(), p.events()
+    kinds = collections.Counter(e["kind"] for e in ev)
+    assert kinds[0] == 2 * 4 and kinds[1] == 2 * 4  # 8 AllGathers (qkv, ffn1) + 8 reduce-scatters
+    assert all(e["executed"] for e in ev)
+    assert s["bytes_total"] < base["bytes_total"]
+    _, bundles, ops, _ = g.export()
+    mm = {bundles[m["acc_bundle"]].tag.decode().split(".")[1]: MODES[m["executed"]] for m in p.matmuls()}
+    assert mm == {"qkv": "gather_inputs", "out_proj": "reduce_outputs", "ffn1": "gather_inputs",
+                  "ffn2": "reduce_outputs"}
+    for e in ev:
+        if e["kind"] == 0:
+            assert e["bytes_per_device"] == (e["lane_count"] // 2) * e["level"] * 2 * LIMB
