@@ -53,6 +53,8 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
   gather_acc.assign(nb, 0);
   full_tg.assign(nb, 0);
   gather_src.assign(nb, 0);
+  gather_lane0.assign(nb, 0);
+  gather_cin.assign(nb, 0);
   first_pmult.assign(nb, -1);
   for (size_t i = 0; i < g.ops.size(); ++i)
     if (g.ops[i].kind == hp::HeOpKind::kPMult && first_pmult[g.ops[i].out.bundle] < 0)
@@ -64,11 +66,25 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
       gather_acc[b] = 1;
       const hp::HeOp& pm0 = g.ops[first_pmult[b]];
       const u32 x = pm0.ins[0].bundle;
+      const PcmmShape sh = pcmm_shape(pm0.ins[0].lane_count, pm0.out.lane_count, pm0.ins[1].lane_count,
+                                      g.bundles[b].chunk_period);
       full_tg[x] = 1;
-      gather_src[x] = 1;
       for (const hp::HeOp& op : g.ops)
         if (op.kind == hp::HeOpKind::kRot && op.ins[0].bundle == x && op.app_node == pm0.app_node)
           full_tg[op.out.bundle] = 1;
+      // "send before bootstrapping": when the activation is a
+      // boot output, gather the boot's input (fewer limbs) and run the boot on
+      // every lane of the group instead
+      int64_t prod = -1;
+      for (int64_t i = 0; i < first_pmult[b]; ++i)
+        if (g.ops[i].out.bundle == x) prod = i;
+      const bool via_boot = prod >= 0 && g.ops[prod].kind == hp::HeOpKind::kBoot &&
+                            g.ops[prod].ins[0].lane_count == g.ops[prod].out.lane_count &&
+                            g.ops[prod].out.lane <= pm0.ins[0].lane;
+      const u32 src = via_boot ? g.ops[prod].ins[0].bundle : x;
+      gather_src[src] = 1;
+      gather_lane0[src] = via_boot ? g.ops[prod].ins[0].lane + (pm0.ins[0].lane - g.ops[prod].out.lane) : pm0.ins[0].lane;
+      gather_cin[src] = sh.c_in;
     }
   }
   if (o.hash_lanes && o.shard) throw Error(AEGIS_EINVAL, "hash lane selection applies to unsharded runs only");
@@ -155,15 +171,10 @@ void Executor::allgather(u32 x) {
   gather_src[x] = 0;
   const ShardPlan& P = *o.shard;
   Bundle& X = *buf[x];
-  int64_t pm = -1;
-  for (size_t b = 0; b < g.bundles.size() && pm < 0; ++b)
-    if (gather_acc[b] && g.ops[first_pmult[b]].ins[0].bundle == x) pm = first_pmult[b];
-  const hp::HeOp& op = g.ops[pm];
-  const PcmmShape sh = pcmm_shape(op.ins[0].lane_count, op.out.lane_count, op.ins[1].lane_count,
-                                  g.bundles[op.out.bundle].chunk_period);
-  if (sh.c_in % P.m) throw Error(AEGIS_EINVAL, "PCMM inputs do not split evenly over the ranks of a token group");
+  const u32 c_in = gather_cin[x];
+  if (c_in % P.m) throw Error(AEGIS_EINVAL, "PCMM inputs do not split evenly over the ranks of a token group");
   const size_t words_per_lane = (size_t)X.comps * X.level * c.n;
-  const size_t share = (size_t)(sh.c_in / P.m) * words_per_lane;
+  const size_t share = (size_t)(c_in / P.m) * words_per_lane;
   cudaEvent_t ready, done;
   AEGIS_CHECK_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   AEGIS_CHECK_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
@@ -172,7 +183,7 @@ void Executor::allgather(u32 x) {
   AEGIS_CHECK_CUDA(cudaEventRecord(ready, c.stream));
   AEGIS_CHECK_CUDA(cudaStreamWaitEvent(c.comm, ready, 0));
   if (o.fault != 1) {
-    p2p_allgather(*o.p2p, X.view().limb(op.ins[0].lane + P.tg_lo * sh.c_in, 0, 0, c.n), share, c.comm);
+    p2p_allgather(*o.p2p, X.view().limb(gather_lane0[x] + P.tg_lo * c_in, 0, 0, c.n), share, c.comm);
     c.count(4);
     comm_bytes += (size_t)(P.m - 1) * share * 8;
   }
@@ -630,6 +641,7 @@ void Executor::step(const hp::HeOp& op, int64_t i) {
           break;
         }
         case K::kBoot: {
+          if (gather_src[op.ins[0].bundle] && full_tg[op.out.bundle]) allgather(op.ins[0].bundle);
           Bundle& in = input(op.ins[0]);
           c.op_boot(get(op.out.bundle), op.out.lane + pos, in, sub_map(op.ins[0], n, pos, len), len, L,
                     g.bundles[op.out.bundle].level);

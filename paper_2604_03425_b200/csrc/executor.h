@@ -104,6 +104,7 @@ class Executor {
   std::vector<u32> alloc_comps, cur_comps;
   std::vector<char> zero_first, partial, donated, is_weight;
   std::vector<char> gather_acc, full_tg, gather_src;  // reference_modes bookkeeping (see RunOptions)
+  std::vector<u32> gather_lane0, gather_cin;          // gathered bundle: lane of (tg 0, pos 0), lanes per tg
   std::vector<int64_t> first_pmult;
   std::vector<int64_t> last_use, last_pmult;
   struct Pending {

@@ -68,7 +68,7 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
       gather[b] = 1;
       const hp::HeOp& pm0 = g.ops[first_pmult[b]];
       const uint32_t x = pm0.ins[0].bundle;
-      full_tg[x] = 1;
+      full_tg[x] = 1;  // (when x is a boot output the boot runs on every lane of the group)
       for (const hp::HeOp& op : g.ops)
         if (op.kind == K::kRot && op.ins[0].bundle == x && op.app_node == pm0.app_node) full_tg[op.out.bundle] = 1;
     }
@@ -150,10 +150,22 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
         for (const hp::LaneSlice& s : g.ops[i].ins)
           if (s.bundle == b) reader = (int64_t)i;
       if (gather[b]) {  // one AllGather of the activation per token group
-        const uint32_t x = pm0.ins[0].bundle;
-        int64_t producer_op = -1;  // the last writer of x before the matmul
+        uint32_t x = pm0.ins[0].bundle, lane0 = pm0.ins[0].lane;
+        int64_t producer_op = -1, reader_op = first_pmult[b];  // last writer of x before the matmul
         for (int64_t i = 0; i < first_pmult[b]; ++i)
           if (g.ops[i].out.bundle == x && g.ops[i].kind != K::kEncode) producer_op = i;
+        // send before bootstrapping: the boot's input is shipped, the boot runs on every lane
+        if (producer_op >= 0 && g.ops[producer_op].kind == K::kBoot &&
+            g.ops[producer_op].ins[0].lane_count == g.ops[producer_op].out.lane_count &&
+            g.ops[producer_op].out.lane <= lane0) {
+          const hp::HeOp& bo = g.ops[producer_op];
+          reader_op = producer_op;
+          lane0 = bo.ins[0].lane + (lane0 - bo.out.lane);
+          x = bo.ins[0].bundle;
+          producer_op = -1;
+          for (int64_t i = 0; i < reader_op; ++i)
+            if (g.ops[i].out.bundle == x && g.ops[i].kind != K::kEncode) producer_op = i;
+        }
         for (uint32_t t = 0; t < tg_total; ++t) {
           PlanEvent e;
           e.id = (uint32_t)P.events.size();
@@ -162,7 +174,7 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
           e.dev_lo = t * m;
           e.dev_count = m;
           e.bundle = x;
-          e.lane = pm0.ins[0].lane + t * sh.c_in;
+          e.lane = lane0 + t * sh.c_in;
           e.lane_count = sh.c_in;
           e.level = g.bundles[x].level;
           e.comps = comps_alloc(x);
@@ -175,7 +187,7 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
           for (uint32_t dd = e.dev_lo; dd < e.dev_lo + m; ++dd) {
             e.trigger_pos.push_back(producer_op >= 0 && last_pos[dd].count(producer_op) ? last_pos[dd].at(producer_op)
                                                                                         : 0);
-            const uint32_t w = first_pos[dd].count(first_pmult[b]) ? first_pos[dd].at(first_pmult[b]) : UINT32_MAX;
+            const uint32_t w = first_pos[dd].count(reader_op) ? first_pos[dd].at(reader_op) : UINT32_MAX;
             e.wait_pos.push_back(w);
             if (w != UINT32_MAX && P.devices[dd].compute[w].wait_event < 0)
               P.devices[dd].compute[w].wait_event = (int32_t)e.id;
