@@ -62,9 +62,10 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
   if (o.reference_modes && o.shard && o.shard->m > 1) {
     if (!o.p2p) throw Error(AEGIS_EINVAL, "matmul reference modes need a p2p window (aegis_graph_set_p2p)");
     for (size_t b = 0; b < nb; ++b) {
-      if (first_pmult[b] < 0 || !gather_executed(g, (u32)b, (u32)first_pmult[b])) continue;
+      const int64_t act = first_pmult[b] < 0 ? -1 : pcmm_activation_op(g, (u32)b);
+      if (act < 0 || !gather_executed(g, (u32)b, (u32)act)) continue;
       gather_acc[b] = 1;
-      const hp::HeOp& pm0 = g.ops[first_pmult[b]];
+      const hp::HeOp& pm0 = g.ops[act];
       const u32 x = pm0.ins[0].bundle;
       const PcmmShape sh = pcmm_shape(pm0.ins[0].lane_count, pm0.out.lane_count, pm0.ins[1].lane_count,
                                       g.bundles[b].chunk_period);
@@ -75,8 +76,12 @@ Executor::Executor(Context& ctx, const hp::HeOpGraph& graph, const RunOptions& o
       // "send before bootstrapping": when the activation is a
       // boot output, gather the boot's input (fewer limbs) and run the boot on
       // every lane of the group instead
-      int64_t prod = -1;
-      for (int64_t i = 0; i < first_pmult[b]; ++i)
+      int64_t prod = -1, first_read = (int64_t)g.ops.size();  // producer: the last writer before the matmul reads x
+      for (size_t i = 0; i < g.ops.size(); ++i)
+        if (g.ops[i].app_node == pm0.app_node)
+          for (const hp::LaneSlice& sl : g.ops[i].ins)
+            if (sl.bundle == x) first_read = std::min(first_read, (int64_t)i);
+      for (int64_t i = 0; i < first_read; ++i)
         if (g.ops[i].out.bundle == x) prod = i;
       const bool via_boot = prod >= 0 && g.ops[prod].kind == hp::HeOpKind::kBoot &&
                             g.ops[prod].ins[0].lane_count == g.ops[prod].out.lane_count &&

@@ -20,6 +20,16 @@ CommCategory category_of(const std::string& tag) {  // comm_plan.hpp:36-49 by ap
   return CommCategory::kOther;
 }
 
+int64_t pcmm_activation_op(const hp::HeOpGraph& g, uint32_t acc) {
+  std::vector<char> rot_out(g.bundles.size(), 0);
+  for (const hp::HeOp& op : g.ops)
+    if (op.kind == K::kRot) rot_out[op.out.bundle] = 1;
+  for (size_t i = 0; i < g.ops.size(); ++i)
+    if (g.ops[i].kind == K::kPMult && g.ops[i].out.bundle == acc && !rot_out[g.ops[i].ins[0].bundle])
+      return (int64_t)i;
+  return -1;
+}
+
 bool gather_executed(const hp::HeOpGraph& g, uint32_t acc, uint32_t first_pmult_op) {
   const hp::HeOp& pm = g.ops[first_pmult_op];
   const PcmmShape sh = pcmm_shape(pm.ins[0].lane_count, pm.out.lane_count, pm.ins[1].lane_count,
@@ -64,9 +74,10 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
     if (op.kind == K::kCMult) cmult_out[op.out.bundle] = 1;
   if (reference_modes && P.m > 1 && P.executable)
     for (size_t b = 0; b < g.bundles.size(); ++b) {
-      if (first_pmult[b] < 0 || !gather_executed(g, (uint32_t)b, (uint32_t)first_pmult[b])) continue;
+      const int64_t act = first_pmult[b] < 0 ? -1 : pcmm_activation_op(g, (uint32_t)b);
+      if (act < 0 || !gather_executed(g, (uint32_t)b, (uint32_t)act)) continue;
       gather[b] = 1;
-      const hp::HeOp& pm0 = g.ops[first_pmult[b]];
+      const hp::HeOp& pm0 = g.ops[act];
       const uint32_t x = pm0.ins[0].bundle;
       full_tg[x] = 1;  // (when x is a boot output the boot runs on every lane of the group)
       for (const hp::HeOp& op : g.ops)
@@ -119,7 +130,8 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
   // ---- matmuls: mode analysis + the executed reduce-scatter events ----------
   for (size_t b = 0; b < g.bundles.size(); ++b) {
     if (first_pmult[b] < 0) continue;
-    const hp::HeOp& pm0 = g.ops[first_pmult[b]];
+    const int64_t act = pcmm_activation_op(g, (uint32_t)b);
+    const hp::HeOp& pm0 = g.ops[act >= 0 ? act : first_pmult[b]];
     const hp::HeOp& pml = g.ops[last_pmult[b]];
     MatmulInfo mi;
     mi.app_node = pm0.app_node;
@@ -151,8 +163,13 @@ ExecPlan build_plan(const hp::HeOpGraph& g, uint32_t tg_total, uint32_t world, u
           if (s.bundle == b) reader = (int64_t)i;
       if (gather[b]) {  // one AllGather of the activation per token group
         uint32_t x = pm0.ins[0].bundle, lane0 = pm0.ins[0].lane;
-        int64_t producer_op = -1, reader_op = first_pmult[b];  // last writer of x before the matmul
-        for (int64_t i = 0; i < first_pmult[b]; ++i)
+        int64_t reader_op = (int64_t)g.ops.size();  // the matmul's first op reading x (any order)
+        for (size_t i = 0; i < g.ops.size(); ++i)
+          if (g.ops[i].app_node == pm0.app_node)
+            for (const hp::LaneSlice& sl : g.ops[i].ins)
+              if (sl.bundle == x) reader_op = std::min(reader_op, (int64_t)i);
+        int64_t producer_op = -1;  // last writer of x before the matmul
+        for (int64_t i = 0; i < reader_op; ++i)
           if (g.ops[i].out.bundle == x && g.ops[i].kind != K::kEncode) producer_op = i;
         // send before bootstrapping: the boot's input is shipped, the boot runs on every lane
         if (producer_op >= 0 && g.ops[producer_op].kind == K::kBoot &&

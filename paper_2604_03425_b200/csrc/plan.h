@@ -95,6 +95,10 @@ ExecPlan build_plan(const heplan::HeOpGraph& g, uint32_t tg_total, uint32_t worl
 // the executed choice for the accumulator `acc` when reference_modes is on:
 // gather iff c_in * level(activation) <= c_out * level(acc)
 bool gather_executed(const heplan::HeOpGraph& g, uint32_t acc, uint32_t first_pmult_op);
+// the PMult of accumulator `acc` that reads the activation itself (its r = 0
+// diagonal: the input is not a rotation output) -- independent of op order,
+// so staggered graphs (aegis_graph_from_plan) resolve the same activation; -1 if none
+int64_t pcmm_activation_op(const heplan::HeOpGraph& g, uint32_t acc);
 CommCategory category_of(const std::string& bundle_tag);
 
 }  // namespace aegis

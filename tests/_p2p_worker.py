@@ -24,6 +24,8 @@ def main():
     kind = int(os.environ.get("P2P_KIND", "0"))  # 1: the FFN graph (splittable at small T)
     c = Context(log_n=11)
     g = c.graph(kind=kind, tokens=tokens)
+    if os.environ.get("P2P_STAGGER") == "1":  # this rank's staggered diagonal order (as bench.py runs ranks)
+        g = g.in_plan_order(g.plan(ws, reorder=True), rank)
     g.set_shard(ws, rank)
     info = g.shard_info()
     groups, m = token_group_comms(ws, info["tg_total"])

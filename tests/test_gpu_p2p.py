@@ -25,16 +25,17 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,tokens,mode,kind,modes", [(8, 64, "device", 0, 0), (16, 64, "device", 0, 0),
-                                                         (8, 64, "hook", 0, 0), (2, 16, "device", 1, 0),
-                                                         (8, 64, "device", 0, 1), (2, 16, "device", 1, 1)])
-def test_p2p_reduce_scatter_processes(world, tokens, mode, kind, modes):
+@pytest.mark.parametrize("world,tokens,mode,kind,modes,stagger", [
+    (8, 64, "device", 0, 0, 0), (16, 64, "device", 0, 0, 0), (8, 64, "hook", 0, 0, 0), (2, 16, "device", 1, 0, 0),
+    (8, 64, "device", 0, 1, 0), (2, 16, "device", 1, 1, 0), (8, 64, "device", 0, 0, 1), (8, 64, "device", 0, 1, 1)])
+def test_p2p_reduce_scatter_processes(world, tokens, mode, kind, modes, stagger):
     """mode device: the executor's comm-stream exchange with flags in the IPC
     windows (no Python in the layer); hook: the host-synchronised reducer.
     kind 1: the FFN graph at T = 16 -- one token group split over 2 ranks.
     modes 1: matmuls gather or reduce as the reference's byte rule picks
     (all-gathers of the activation on the comm stream)."""
-    env = dict(os.environ, P2P_TOKENS=str(tokens), P2P_MODE=mode, P2P_KIND=str(kind), P2P_MODES=str(modes))
+    env = dict(os.environ, P2P_TOKENS=str(tokens), P2P_MODE=mode, P2P_KIND=str(kind), P2P_MODES=str(modes),
+               P2P_STAGGER=str(stagger))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "_p2p_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
