@@ -411,6 +411,10 @@ int aegis_graph_set_wrap_defer(aegis_graph* g, int enable);
 /* per-op device times (CUDA events around every HeOp) of the next runs */
 int aegis_graph_set_profiling(aegis_graph* g, int enable);
 int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t* n);
+/* the two-stream trace of the last profiled run: every comm-stream exchange
+ * as (start ms, end ms, bundle id) triples relative to the run's first
+ * compute-stream event (op i spans [sum of op_times[<i], sum[<=i]]) */
+int aegis_graph_comm_times(const aegis_graph* g, float* out, uint64_t cap, uint64_t* n);
 /* bytes copied host->device / device->host by the last aegis_graph_run_host */
 int aegis_graph_io_bytes(const aegis_graph* g, uint64_t* h2d, uint64_t* d2h);
 /* Execute ops [0, max_ops) (all if < 0).  Bundles are allocated at first write

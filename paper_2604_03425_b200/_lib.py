@@ -159,6 +159,7 @@ SIGNATURES = [
     ("aegis_graph_set_wrap_defer", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_graph_set_profiling", ctypes.c_int, [vp, ctypes.c_int]),
     ("aegis_graph_op_times", ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_float), u64, u64p]),
+    ("aegis_graph_comm_times", ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_float), u64, u64p]),
     ("aegis_graph_io_bytes", ctypes.c_int, [vp, u64p, u64p]),
     ("aegis_graph_run", ctypes.c_int, [vp, vp, i64, u64p, u64]),
     ("aegis_graph_io_words", ctypes.c_int, [vp, u64p, u64p]),

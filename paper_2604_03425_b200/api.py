@@ -482,6 +482,15 @@ class Graph:
                                       ctypes.byref(n))
         return a
 
+    def comm_times(self):
+        """Two-stream trace of the last profiled run: (start ms, end ms, bundle) per exchange."""
+        n = ctypes.c_uint64()
+        self.lib.aegis_graph_comm_times(self.h, None, 0, ctypes.byref(n))
+        a = np.zeros(3 * max(1, n.value), dtype=np.float32)
+        self.lib.aegis_graph_comm_times(self.h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n.value,
+                                        ctypes.byref(n))
+        return [(float(a[3 * i]), float(a[3 * i + 1]), int(a[3 * i + 2])) for i in range(n.value)]
+
     def io_bytes(self):
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         self.lib.aegis_graph_io_bytes(self.h, ctypes.byref(a), ctypes.byref(b))

@@ -103,6 +103,7 @@ struct aegis_graph {
   uint64_t h2d = 0, d2h = 0, comm = 0;
   bool profile = false;
   std::vector<float> op_ms;
+  std::vector<float> comm_trace;
 };
 
 namespace {
@@ -131,7 +132,10 @@ void run_graph(aegis_ctx* ctx, aegis_graph* g, aegis::RunOptions opt) {
   opt.hoist = g->hoist != 0;
   opt.dce = g->dce != 0;
   opt.wrap_defer = g->wrap_defer != 0;
-  if (g->profile) opt.op_ms = &g->op_ms;
+  if (g->profile) {
+    opt.op_ms = &g->op_ms;
+    opt.comm_trace = &g->comm_trace;
+  }
   // no trim here: the arena keeps its mapping across runs (re-mapping ~130 GB
   // per layer run stalled the stream); key allocation trims on demand
   c.peak_bytes = c.live_bytes;
@@ -1073,6 +1077,14 @@ int aegis_graph_op_times(const aegis_graph* g, float* ms, uint64_t cap, uint64_t
   if (!g) return AEGIS_EINVAL;
   for (size_t i = 0; i < g->op_ms.size() && i < cap; ++i) ms[i] = g->op_ms[i];
   if (n) *n = g->op_ms.size();
+  return AEGIS_OK;
+}
+int aegis_graph_comm_times(const aegis_graph* g, float* out, uint64_t cap, uint64_t* n) {
+  if (!g) return AEGIS_EINVAL;
+  const size_t k = g->comm_trace.size() / 3;
+  for (size_t i = 0; i < k && i < cap && out; ++i)
+    for (int j = 0; j < 3; ++j) out[3 * i + j] = g->comm_trace[3 * i + j];
+  if (n) *n = k;
   return AEGIS_OK;
 }
 int aegis_graph_set_dce(aegis_graph* g, int enable) {

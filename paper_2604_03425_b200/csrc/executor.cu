@@ -169,6 +169,19 @@ Bundle& Executor::input(const hp::LaneSlice& s, u32 lo, u32 hi) {
   return *buf[s.bundle];
 }
 
+void Executor::comm_mark_begin(u32 b) {
+  if (!o.comm_trace) return;
+  CommMark m{nullptr, nullptr, b};
+  AEGIS_CHECK_CUDA(cudaEventCreate(&m.start));
+  AEGIS_CHECK_CUDA(cudaEventCreate(&m.end));
+  AEGIS_CHECK_CUDA(cudaEventRecord(m.start, c.comm));
+  comm_marks.push_back(m);
+}
+void Executor::comm_mark_end() {
+  if (!o.comm_trace || comm_marks.empty()) return;
+  AEGIS_CHECK_CUDA(cudaEventRecord(comm_marks.back().end, c.comm));
+}
+
 // Gather-mode activation: the m ranks of the token group each computed their
 // own part of its lanes; one all-gather on the comm stream fills the rest.
 // Issued at the matmul's first read (the r = 0 PMult), waited on at once.
@@ -188,7 +201,9 @@ void Executor::allgather(u32 x) {
   AEGIS_CHECK_CUDA(cudaEventRecord(ready, c.stream));
   AEGIS_CHECK_CUDA(cudaStreamWaitEvent(c.comm, ready, 0));
   if (o.fault != 1) {
+    comm_mark_begin(x);
     p2p_allgather(*o.p2p, X.view().limb(gather_lane0[x] + P.tg_lo * c_in, 0, 0, c.n), share, c.comm);
+    comm_mark_end();
     c.count(4);
     comm_bytes += (size_t)(P.m - 1) * share * 8;
   }
@@ -473,7 +488,9 @@ void Executor::reduce_async(u32 b) {
   for (u32 s = 0; s < sh.S; ++s) {
     const u32 lane0 = pm.out.lane + pcmm_lane(sh, t, s * sh.c_sub);
     if (o.fault != 1) {
+      comm_mark_begin(b);
       p2p_exchange(*o.p2p, acc.view().limb(lane0, 0, 0, c.n), words_per_lane * share, c.comm);
+      comm_mark_end();
       c.count(4);
       comm_bytes += (size_t)(P.m - 1) * words_per_lane * share * 8;
     }
@@ -751,8 +768,21 @@ void Executor::run() {
     }
   if (o.op_ms) {
     AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.stream));
+    AEGIS_CHECK_CUDA(cudaStreamSynchronize(c.comm));
     o.op_ms->assign(nops, 0.0f);
     for (int64_t i = 0; i < nops; ++i) cudaEventElapsedTime(&(*o.op_ms)[i], ev[i], ev[i + 1]);
+    if (o.comm_trace) {
+      o.comm_trace->clear();
+      for (const CommMark& m : comm_marks) {
+        float s0 = 0, s1 = 0;
+        cudaEventElapsedTime(&s0, ev[0], m.start);
+        cudaEventElapsedTime(&s1, ev[0], m.end);
+        o.comm_trace->insert(o.comm_trace->end(), {s0, s1, (float)m.bundle});
+        cudaEventDestroy(m.start);
+        cudaEventDestroy(m.end);
+      }
+      comm_marks.clear();
+    }
     for (auto& e : ev) cudaEventDestroy(e);
   }
 }

@@ -51,6 +51,9 @@ struct RunOptions {
   bool dce = false;  // skip output lanes no later op reads (final bundle unchanged)
   bool wrap_defer = true;  // wrapped accumulating CAdds summed at the operand's width (bit-identical)
   std::vector<float>* op_ms = nullptr;  // if set: per-op device time (CUDA events)
+  // if set (with op_ms): every comm-stream exchange as (start ms, end ms, bundle)
+  // relative to the run's first compute-stream event -- the two-stream trace
+  std::vector<float>* comm_trace = nullptr;
 };
 
 class Executor {
@@ -113,6 +116,13 @@ class Executor {
   };
   std::vector<std::vector<Pending>> pending;  // comm-stream exchanges not yet waited for
   std::vector<cudaEvent_t> events;            // every event this run created (destroyed at the end)
+  struct CommMark {
+    cudaEvent_t start, end;
+    u32 bundle;
+  };
+  std::vector<CommMark> comm_marks;  // comm_trace: timed exchanges
+  void comm_mark_begin(u32 bundle);
+  void comm_mark_end();
   std::vector<Group> groups;
   std::vector<int> group_of;
   std::vector<std::vector<char>> live;  // dce: [bundle][lane] read by a later op (or final)

@@ -40,7 +40,20 @@ def main():
         if mode == "collective":  # the torch.distributed path, for comparison
             red.fallback = make_reducer(groups, rank % m)
         g.set_reducer(red)
+    trace = os.environ.get("P2P_TRACE") == "1"
+    if trace:  # two-stream trace: the exchanges on the comm stream against the compute-stream ops
+        g.set_profiling(True)
     h = g.run(hashes=True)
+    if trace and rank == 0:
+        ops = np.cumsum(np.concatenate([[0.0], g.op_times()]))
+        _, bundles, opd, _ = g.export()
+        for s0, s1, b in g.comm_times():
+            busy = [(i, max(ops[i], s0), min(ops[i + 1], s1)) for i in range(len(ops) - 1)
+                    if ops[i] < s1 and ops[i + 1] > s0]
+            kinds = sorted({("encode", "padd", "cadd", "pmult", "cmult", "rot", "relin", "rescale", "boot")[opd[i].kind]
+                            for i, _, _ in busy})
+            print(f"TRACE exchange {bundles[b].tag.decode():28s} comm [{s0:9.3f}, {s1:9.3f}] ms; compute ops during it: "
+                  f"{len(busy)} ({', '.join(kinds)}), first op {busy[0][0] if busy else -1}", flush=True)
     hs = [None] * ws
     dist.all_gather_object(hs, h.tolist())
     sent = [None] * ws
